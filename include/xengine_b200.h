@@ -1,0 +1,257 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * xengine_b200 — C ABI of the B200-native XEngine hot path.
+ *
+ * The reference (arXiv 2212.09290, /root/reference/proj) is a pure C++20
+ * library with no FFI layer; its public API lives in proj/include/xengine/ (one .hpp per module).
+ * Every entry point below replaces one reference function (or the inner loop
+ * of one) and says which, as file:line under proj/.  The C++ mirror of the
+ * reference API (include/xengine/b200.hpp) and the Python bindings
+ * (paper_2212_09290_b200/_lib.py) are thin layers over these symbols.
+ *
+ * Conventions
+ *   - Every function returns int status: XE_OK (0), or an xengine::Errc value
+ *     + 1 (proj/include/xengine/errors.hpp:9-42), or XE_ERR_CUDA / XE_ERR_NCCL /
+ *     XE_ERR_ARG.  xe_last_error() returns the thread-local message.
+ *   - No exceptions cross this boundary; plain pointers and sizes only.
+ *   - Handles are immutable after construction and bound to one CUDA stream.
+ *   - Buffers documented "device" must be device pointers (cudaMalloc / torch
+ *     CUDA tensors); "host" buffers may be pageable or pinned.
+ */
+#ifndef XENGINE_B200_H
+#define XENGINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  XE_OK = 0,
+  /* 1 + xengine::Errc (errors.hpp:9-42) */
+  XE_ERR_MALFORMED_DOCUMENT = 1,
+  XE_ERR_NON_TOPOLOGICAL_EDGE = 2,
+  XE_ERR_UNKNOWN_DEVICE = 3,
+  XE_ERR_NON_POSITIVE_SIZE = 4,
+  XE_ERR_NEGATIVE_COST = 5,
+  XE_ERR_EMPTY_NETWORK = 6,
+  XE_ERR_PERCENT_OUT_OF_RANGE = 7,
+  XE_ERR_MISSING_LINK = 8,
+  XE_ERR_DIMENSION_MISMATCH = 9,
+  XE_ERR_INCOMPLETE_ENERGY_TABLE = 10,
+  XE_ERR_UNKNOWN_VARIABLE = 11,
+  XE_ERR_NON_INTEGRAL_BINARY = 12,
+  XE_ERR_EMPTY_SOLUTION = 13,
+  XE_ERR_INFEASIBLE_MARKER = 14,
+  XE_ERR_INFEASIBLE_PROBLEM = 15,
+  XE_ERR_TOO_LARGE = 16,
+  XE_ERR_EXTERNAL_SOLVER_UNAVAILABLE = 17,
+  XE_ERR_SOLVER_FAILED = 18,
+  XE_ERR_UNPARSABLE_SOLUTION = 19,
+  XE_ERR_OBJECTIVE_MISMATCH = 20,
+  XE_ERR_ILLEGAL_ASSIGNMENT = 21,
+  XE_ERR_ILLEGAL_SCHEDULE = 22,
+  XE_ERR_EMPTY_SERIES = 23,
+  XE_ERR_NON_POSITIVE_TIME = 24,
+  XE_ERR_IO = 25,
+  /* boundary-only */
+  XE_ERR_CUDA = 100,
+  XE_ERR_NCCL = 101,
+  XE_ERR_ARG = 102,
+  XE_ERR_NO_DEVICE = 103
+};
+
+/* ---- K2 validity bits --------------------------------------------------
+ * One bit per constraint family of check_assignment (model.cpp:430-469) on
+ * the completion of (R,S) (model.cpp:471-549); bits 0..14 non-zero <=>
+ * check_assignment(build_model(p,opts), complete_assignment(p,opts,R,S))
+ * returns a non-empty list.  On a completion only FIXED_ZERO, EQ8, EQ9,
+ * EQ11, EQ12, EQ16_HI, ENERGY_* and U_BOUND can fire; the others hold by
+ * construction and are listed for completeness. */
+enum {
+  XE_F_FIXED_ZERO = 1u << 0,   /* R(d,t,i>t) or S(d,t,i>=t) set (model.cpp:126-132) */
+  XE_F_EQ8 = 1u << 1,          /* diagonal not on exactly one device */
+  XE_F_EQ9 = 1u << 2,          /* total diagonal count != T */
+  XE_F_EQ11 = 1u << 3,         /* S(d,t+1,i) > S(d,t,i)+R(d,t,i) */
+  XE_F_EQ12 = 1u << 4,         /* computed op with a parent resident nowhere */
+  XE_F_EQ13 = 1u << 5,
+  XE_F_EQ14 = 1u << 6,
+  XE_F_EQ16_LO = 1u << 7,
+  XE_F_EQ16_HI = 1u << 8,      /* hazard row (only together with EQ11) */
+  XE_F_Z_LINK = 1u << 9,
+  XE_F_P_LINK = 1u << 10,
+  XE_F_ENERGY_DEV = 1u << 11,
+  XE_F_ENERGY_TOTAL = 1u << 12,
+  XE_F_U_BOUND = 1u << 13,     /* U > b(1+tol)+tol, tol = 1e-6 (model.cpp:441-445) */
+  XE_F_OTHER = 1u << 14,       /* binary / P range / space (never on a completion) */
+  XE_F_BUDGET = 1u << 15,      /* integer peak_d > b_d (solver.cpp:237,249; schedule.cpp:181) */
+  XE_F_DECODE = 1u << 16,      /* decode() raises IllegalAssignment (schedule.cpp:63-71) */
+  XE_F_DECODE_FREED = 1u << 17 /* some copy source was freed earlier in its timestep */
+};
+#define XE_F_CHECK_MASK 0x7fffu
+
+/* ---- problem ----------------------------------------------------------- */
+/* Structure-of-arrays image of xengine::Problem (problem.hpp:18-60) after
+ * copy_cost (problem.cpp:358-380) has been applied to every (edge, ds, dc). */
+typedef struct xe_problem_desc {
+  int32_t D, T, E;
+  const int64_t* output_bytes; /* [T] */
+  const double* cost_ms;       /* [D][T]  (device-major) */
+  const int32_t* edge_src;     /* [E] edge declaration order */
+  const int32_t* edge_dst;     /* [E] */
+  const double* copy_ms;       /* [E][D][D]; diagonal ignored */
+  const int64_t* budget_bytes; /* [D] */
+  /* optional energy model (model.hpp:50-56); has_energy = 0 -> none */
+  int32_t has_energy;
+  double alpha;
+  const double* q_joules;        /* [D][T] */
+  const uint8_t* has_dev_limit;  /* [D] */
+  const double* dev_limit;       /* [D] */
+  int32_t has_total_limit;
+  double total_limit;
+  double board_joules;
+} xe_problem_desc;
+
+typedef struct xe_problem xe_problem; /* opaque; owns device copies */
+
+typedef struct xe_model_opts {
+  int32_t strict_free;         /* ModelOptions::strict_free (model.hpp:58-62) */
+  int32_t quadratic_objective; /* ModelOptions::quadratic_objective */
+  int32_t use_energy;          /* apply the problem's energy model (add_energy_extension) */
+} xe_model_opts;
+
+const char* xe_last_error(void);
+const char* xe_version(void);
+
+/* Parses a problem document (load_problem, problem.cpp:228-244, including the
+ * layered training-graph form, problem.cpp:190-224/280-338) and the optional
+ * energy section (parse_energy, model.cpp:314-367) on the host, then uploads. */
+int xe_problem_load_json(const char* json_text, int device, xe_problem** out);
+/* Uploads an already-resolved problem (validate_problem, problem.cpp:254-278). */
+int xe_problem_create(const xe_problem_desc* desc, int device, xe_problem** out);
+int xe_problem_destroy(xe_problem* p);
+/* Host view of the resolved arrays (pointers stay valid for the handle's life). */
+int xe_problem_describe(const xe_problem* p, xe_problem_desc* out);
+/* with_budgets (problem.cpp:382-393): new handle, same problem, new budgets. */
+int xe_problem_with_budgets(const xe_problem* p, const int64_t* budgets, xe_problem** out);
+
+/* ---- K1: MILP assembly (build_model, model.cpp:86-312) ------------------ */
+typedef struct xe_csr xe_csr; /* opaque; device-resident model */
+
+typedef struct xe_csr_info {
+  int64_t n_cols;   /* 4DT^2 + DT(E+T) + TED(D-1) (model.hpp:14-31 order) */
+  int64_t n_rows;   /* constraints in emission order */
+  int64_t nnz;
+  int64_t n_rows_mps; /* rows written to MPS (P_LINK dropped when quadratic) */
+  int32_t D, T, E;
+  int32_t n_tags;   /* 14 (ConstraintTag, model.hpp:36-39) */
+  int64_t tag_rows[16]; /* rows per ConstraintTag */
+} xe_csr_info;
+
+/* Device pointers into the model (valid while the handle lives). */
+typedef struct xe_csr_view {
+  const int64_t* row_ptr; /* [n_rows+1] */
+  const int32_t* col;     /* [nnz] column = closed-form VarRef index */
+  const double* val;      /* [nnz] */
+  const double* rhs;      /* [n_rows] */
+  const int8_t* sense;    /* [n_rows] 'L','G','E' */
+  const uint8_t* tag;     /* [n_rows] ConstraintTag */
+  const int32_t* ordinal; /* [n_rows] per-tag ordinal */
+  const double* obj;      /* [n_cols] objective (0 where absent) */
+  const uint8_t* obj_present; /* [n_cols] 1 where the reference map holds an entry */
+  const double* lb;       /* [n_cols] */
+  const double* ub;       /* [n_cols] (FX 0 -> 0, BV -> 1, U -> budget, P -> 1) */
+  const uint8_t* kind;    /* [n_cols] 0 fixed-zero, 1 binary, 2 memory(U), 3 product(P) */
+} xe_csr_view;
+
+int xe_build_csr(const xe_problem* p, const xe_model_opts* opts, xe_csr** out);
+int xe_csr_destroy(xe_csr* m);
+int xe_csr_get_info(const xe_csr* m, xe_csr_info* out);
+int xe_csr_get_view(const xe_csr* m, xe_csr_view* out);
+/* Column-major copy (stable by row) for SpMTV and MPS emission. */
+int xe_csr_build_csc(xe_csr* m);
+int xe_csr_get_csc(const xe_csr* m, const int64_t** col_ptr, const int32_t** row,
+                   const double** val);
+/* Bit-exact write_mps (mps_io.cpp:109-199) of the model.  Two-call: pass
+ * buf = NULL to get the size in *len, then a buffer of *len bytes. */
+int xe_write_mps(xe_csr* m, char* buf, size_t* len);
+/* Time of the last K1 assembly (device, CUDA events), milliseconds. */
+int xe_csr_last_build_ms(const xe_csr* m, float* ms);
+
+/* ---- K2: batched schedule evaluation ----------------------------------- */
+/* Dense cube batch layout ("xe_cube"): candidate-major, per candidate the R
+ * cube then the S cube, each [D][T][W] uint32 words with W = ceil(T/32);
+ * bit i of row (d,t) is word i>>5, bit i&31.  Replaces BitCube
+ * (model.hpp:127-139).  Bytes per candidate: 8*D*T*W. */
+size_t xe_cube_bytes(int32_t D, int32_t T);
+
+typedef struct xe_eval_out {
+  double* obj;      /* [n] objective_value of the completion (model.cpp:369-428) */
+  int64_t* peak;    /* [n][D] max_t,v U(d,t,v) = replay peaks (schedule.cpp:326-367) */
+  uint32_t* flags;  /* [n] XE_F_* bits */
+} xe_eval_out;
+
+typedef struct xe_best {
+  double obj;       /* best objective among candidates with (flags & mask) == 0 */
+  int64_t index;    /* lowest index attaining it (solver.cpp:57-61 tie rule); -1 none */
+  int64_t n_valid;
+} xe_best;
+
+/* Evaluates n candidates.  cubes, out arrays: device pointers.  out may have
+ * NULL members to skip writing them.  best (host, may be NULL) receives the
+ * argmin over candidates whose flags & valid_mask == 0.  stream = 0 -> the
+ * handle's stream. */
+int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
+                  int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best,
+                  void* stream);
+/* Same, host buffers: copies in/out inside the call (the end-to-end path). */
+int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
+                       int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best);
+
+/* Placement candidates: dev[n][T] uint8 device per operator (save_all_assignment,
+ * solver.cpp:30-42).  policy 0 = save-all (the reference's family),
+ * policy 1 = minimal-save (saved only until the last consumer). */
+int xe_eval_placements(const xe_problem* p, const uint8_t* dev, int64_t n, int32_t policy,
+                       xe_eval_out* out, uint32_t valid_mask, xe_best* best, void* stream);
+/* assignment_oracle (solver.cpp:44-75) as a full GPU sweep over D^T
+ * placements in odometer order; writes the winning device vector. */
+int xe_assignment_oracle(const xe_problem* p, double* best_obj, int32_t* best_dev,
+                         int64_t* n_evaluated);
+
+/* ---- K3: PDHG LP relaxation -------------------------------------------- */
+typedef struct xe_pdhg_opts {
+  int32_t max_iters;
+  double tol_rel;           /* relative KKT tolerance (default 1e-6) */
+  int32_t check_every;      /* iterations between convergence checks (default 64) */
+  int32_t verbose;
+  const double* lb_override; /* host [n] or NULL (node bounds for B&B) */
+  const double* ub_override; /* host [n] or NULL */
+} xe_pdhg_opts;
+
+typedef struct xe_pdhg_result {
+  double primal_obj, dual_obj;
+  double rel_gap, rel_primal_res, rel_dual_res;
+  int32_t iters, restarts, status; /* 0 converged, 1 iteration limit */
+  double solve_ms;           /* device time, CUDA events */
+  double spmv_ms_per_iter;
+} xe_pdhg_result;
+
+int xe_pdhg_solve(xe_csr* m, const xe_pdhg_opts* opts, xe_pdhg_result* res,
+                  double* x_out /* host [n] or NULL */, double* y_out /* host [m] or NULL */);
+
+/* ---- K4: randomized rounding + repair ---------------------------------- */
+/* Samples n candidate cubes from LP marginals x (device [n_cols] or NULL for
+ * uniform placements): placement from the R(.,t,t) diagonal, minimal-save S,
+ * up to `edits` drop-and-recompute edits, all valid for EQ8/11/12 by
+ * construction; a fraction `perturb` gets one random bit flip. */
+int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int64_t first,
+                   int64_t n, int32_t edits, double perturb, uint32_t* cubes_dev,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XENGINE_B200_H */
