@@ -130,6 +130,10 @@ const char* xe_version(void);
  * layered training-graph form, problem.cpp:190-224/280-338) and the optional
  * energy section (parse_energy, model.cpp:314-367) on the host, then uploads. */
 int xe_problem_load_json(const char* json_text, int device, xe_problem** out);
+/* Host-only parse (no device touched): a handle on which only
+ * xe_problem_describe / xe_problem_destroy are valid.  Lets host tooling and
+ * CPU tests check the loader without a GPU. */
+int xe_problem_parse_json(const char* json_text, xe_problem** out);
 /* Uploads an already-resolved problem (validate_problem, problem.cpp:254-278). */
 int xe_problem_create(const xe_problem_desc* desc, int device, xe_problem** out);
 int xe_problem_destroy(xe_problem* p);

@@ -1,0 +1,188 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Python mirror of the reference's public API for the hot path.
+
+Names follow proj/include/xengine/*.hpp; every call goes through the C ABI
+(``_lib``) to the sm_100a kernels.  torch is used only for device memory and
+streams.
+
+    reference (C++)                         here
+    load_problem / load_problem_file        Problem.from_json / Problem.from_file
+    with_budgets                            Problem.with_budgets
+    build_model + write_mps                 build_model(...).write_mps()
+    complete_assignment + objective_value   evaluate_cubes(...)  (batched)
+      + check_assignment (+ replay peaks)
+    save_all_assignment + objective_value   evaluate_placements(...)
+    assignment_oracle                       assignment_oracle(...)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import LIB, check
+
+
+@dataclass
+class ModelOptions:
+    """xengine::ModelOptions (model.hpp:58-62); energy=True applies the
+    document's energy section (the reference passes an EnergyModel)."""
+    strict_free: bool = False
+    quadratic_objective: bool = False
+    energy: bool = False
+
+    def c(self):
+        return _lib.ModelOpts(int(self.strict_free), int(self.quadratic_objective), int(self.energy))
+
+
+class Problem:
+    """Device-resident problem handle (xe_problem)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        d = _lib.ProblemDesc()
+        check(LIB.xe_problem_describe(self._h, C.byref(d)))
+        self.D, self.T, self.E = d.D, d.T, d.E
+        self._desc = d
+
+    @classmethod
+    def from_json(cls, text: str, device: int = 0) -> "Problem":
+        h = C.c_void_p()
+        check(LIB.xe_problem_load_json(text.encode(), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_file(cls, path: str, device: int = 0) -> "Problem":
+        try:
+            with open(path) as f:
+                text = f.read()
+        except OSError as ex:
+            raise _lib.XeError(25, f"cannot open {path}: {ex}")
+        return cls.from_json(text, device)
+
+    @classmethod
+    def from_arrays(cls, D, T, E, output_bytes, cost_ms, edge_src, edge_dst, copy_ms,
+                    budget_bytes, device: int = 0, energy=None) -> "Problem":
+        keep = [np.ascontiguousarray(output_bytes, np.int64),
+                np.ascontiguousarray(cost_ms, np.float64),
+                np.ascontiguousarray(edge_src, np.int32), np.ascontiguousarray(edge_dst, np.int32),
+                np.ascontiguousarray(copy_ms, np.float64),
+                np.ascontiguousarray(budget_bytes, np.int64)]
+        d = _lib.ProblemDesc(D, T, E, *[k.ctypes.data for k in keep])
+        if energy is not None:
+            q = np.ascontiguousarray(energy["q"], np.float64)
+            hl = np.ascontiguousarray(energy.get("has_dev_limit", np.zeros(D)), np.uint8)
+            lim = np.ascontiguousarray(energy.get("dev_limit", np.zeros(D)), np.float64)
+            keep += [q, hl, lim]
+            d.has_energy = 1
+            d.alpha = float(energy.get("alpha", 0.0))
+            d.q_joules, d.has_dev_limit, d.dev_limit = q.ctypes.data, hl.ctypes.data, lim.ctypes.data
+            tl = energy.get("total_limit")
+            d.has_total_limit = 0 if tl is None else 1
+            d.total_limit = 0.0 if tl is None else float(tl)
+            d.board_joules = float(energy.get("board_joules", 0.0))
+        h = C.c_void_p()
+        check(LIB.xe_problem_create(C.byref(d), device, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            if self._h:
+                LIB.xe_problem_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def arrays(self) -> dict:
+        """Resolved arrays (after copy_cost) as numpy copies."""
+        d = self._desc
+        D, T, E = self.D, self.T, self.E
+
+        def arr(ptr, n, dt):
+            if n == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(
+                C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), shape=(n,)).copy()
+
+        out = {
+            "output_bytes": arr(d.output_bytes, T, np.int64),
+            "cost_ms": arr(d.cost_ms, D * T, np.float64).reshape(D, T),
+            "edge_src": arr(d.edge_src, E, np.int32),
+            "edge_dst": arr(d.edge_dst, E, np.int32),
+            "copy_ms": arr(d.copy_ms, E * D * D, np.float64).reshape(E, D, D),
+            "budget_bytes": arr(d.budget_bytes, D, np.int64),
+            "has_energy": bool(d.has_energy),
+        }
+        if d.has_energy:
+            out.update(alpha=d.alpha, q_joules=arr(d.q_joules, D * T, np.float64).reshape(D, T),
+                       has_dev_limit=arr(d.has_dev_limit, D, np.uint8),
+                       dev_limit=arr(d.dev_limit, D, np.float64),
+                       total_limit=d.total_limit if d.has_total_limit else None,
+                       board_joules=d.board_joules)
+        return out
+
+    def with_budgets(self, budgets) -> "Problem":
+        b = np.ascontiguousarray(budgets, np.int64)
+        h = C.c_void_p()
+        check(LIB.xe_problem_with_budgets(self._h, b.ctypes.data, C.byref(h)))
+        return Problem(h)
+
+    @property
+    def cube_words(self) -> int:
+        return 2 * self.D * self.T * ((self.T + 31) // 32)
+
+
+@dataclass
+class EvalResult:
+    obj: object       # [n] float64 (torch on device, or numpy)
+    peak: object      # [n, D] int64
+    flags: object     # [n] uint32 (as int32 in torch)
+    best_obj: float
+    best_index: int
+    n_valid: int
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def evaluate_cubes(problem: Problem, cubes, opts: Optional[ModelOptions] = None,
+                   valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True, stream=None):
+    """Evaluate device-resident cubes (torch uint32/int32 CUDA tensor of
+    shape [n, cube_words]).  Returns EvalResult with torch tensors."""
+    import torch
+    opts = opts or ModelOptions()
+    n = cubes.shape[0] if cubes.dim() > 1 else cubes.numel() // problem.cube_words
+    dev = cubes.device
+    obj = torch.empty(n, dtype=torch.float64, device=dev) if outputs else None
+    peak = torch.empty((n, problem.D), dtype=torch.int64, device=dev) if outputs else None
+    flags = torch.empty(n, dtype=torch.int32, device=dev) if outputs else None
+    out = _lib.EvalOut(_ptr(obj), _ptr(peak), _ptr(flags))
+    best = _lib.Best()
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    check(LIB.xe_eval_cubes(problem.handle, C.byref(opts.c()), C.c_void_p(cubes.data_ptr()), n,
+                            C.byref(out), valid_mask, C.byref(best), C.c_void_p(s)))
+    return EvalResult(obj, peak, flags, best.obj, best.index, best.n_valid)
+
+
+def evaluate_cubes_host(problem: Problem, cubes: np.ndarray, opts: Optional[ModelOptions] = None,
+                        valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True):
+    """End-to-end path: host cubes -> host results (copies inside the call)."""
+    opts = opts or ModelOptions()
+    cubes = np.ascontiguousarray(cubes, np.uint32).reshape(-1, problem.cube_words)
+    n = cubes.shape[0]
+    obj = np.empty(n, np.float64) if outputs else None
+    peak = np.empty((n, problem.D), np.int64) if outputs else None
+    flags = np.empty(n, np.uint32) if outputs else None
+    out = _lib.EvalOut(*(None if a is None else C.c_void_p(a.ctypes.data) for a in (obj, peak, flags)))
+    best = _lib.Best()
+    check(LIB.xe_eval_cubes_host(problem.handle, C.byref(opts.c()), cubes.ctypes.data, n,
+                                 C.byref(out), valid_mask, C.byref(best)))
+    return EvalResult(obj, peak, flags, best.obj, best.index, best.n_valid)

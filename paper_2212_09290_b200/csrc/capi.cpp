@@ -1,0 +1,299 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// C ABI (include/xengine_b200.h): handles, error mapping, host<->device
+// plumbing.  No exceptions cross this boundary; every entry is wrapped in
+// xe::guard.  There is no CPU fallback: without a CUDA device every compute
+// entry point returns XE_ERR_NO_DEVICE.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "xe_internal.hpp"
+
+namespace xe {
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+size_t eval_scratch_bytes(int device);
+void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const uint32_t* cubes,
+                       int64_t n, double* obj, int64_t* peak, uint32_t* flags, uint32_t valid_mask,
+                       uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
+
+namespace {
+
+void require_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(XE_ERR_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (device < 0 || device >= n) fail(XE_ERR_ARG, "device index out of range");
+  XE_CUDA(cudaSetDevice(device));
+}
+
+template <class T>
+std::vector<T> vec(const T* p, size_t n) {
+  if (!p && n) fail(XE_ERR_ARG, "null array in problem description");
+  return p ? std::vector<T>(p, p + n) : std::vector<T>();
+}
+
+xe_problem* make_handle(HostProblem&& h, int device) {
+  require_device(device);
+  auto pr = std::make_unique<xe_problem>();
+  pr->device = device;
+  pr->h = std::move(h);
+  XE_CUDA(cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking));
+  upload_problem(pr.get());
+  pr->scratch.alloc(eval_scratch_bytes(device));
+  return pr.release();
+}
+
+}  // namespace
+
+void require_uploaded(const xe_problem* p) {
+  if (p->device < 0) fail(XE_ERR_NO_DEVICE, "host-only problem handle (xe_problem_parse_json)");
+  XE_CUDA(cudaSetDevice(p->device));
+}
+
+namespace {
+
+xe_model_opts opts_or_default(const xe_model_opts* o) {
+  xe_model_opts d{};
+  return o ? *o : d;
+}
+
+void read_best(const uint64_t* dev3, cudaStream_t s, xe_best* best) {
+  uint64_t hb[3];
+  XE_CUDA(cudaMemcpyAsync(hb, dev3, sizeof hb, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaStreamSynchronize(s));
+  best->index = static_cast<int64_t>(hb[1]);
+  best->n_valid = static_cast<int64_t>(hb[2]);
+  double o;
+  std::memcpy(&o, &hb[0], 8);
+  best->obj = best->index >= 0 ? o : INFINITY;
+}
+
+}  // namespace
+}  // namespace xe
+
+using namespace xe;
+
+extern "C" {
+
+const char* xe_last_error(void) { return g_last_error.c_str(); }
+const char* xe_version(void) { return "xengine_b200 0.1 (sm_100a)"; }
+
+size_t xe_cube_bytes(int32_t D, int32_t T) {
+  return static_cast<size_t>(8) * D * T * ((T + 31) / 32);
+}
+
+int xe_problem_load_json(const char* json_text, int device, xe_problem** out) {
+  return guard([&] {
+    if (!json_text || !out) fail(XE_ERR_ARG, "null argument");
+    HostProblem h = load_problem_json(json_text);
+    *out = make_handle(std::move(h), device);
+  });
+}
+
+int xe_problem_parse_json(const char* json_text, xe_problem** out) {
+  return guard([&] {
+    if (!json_text || !out) fail(XE_ERR_ARG, "null argument");
+    auto pr = std::make_unique<xe_problem>();
+    pr->device = -1;
+    pr->h = load_problem_json(json_text);
+    *out = pr.release();
+  });
+}
+
+int xe_problem_create(const xe_problem_desc* d, int device, xe_problem** out) {
+  return guard([&] {
+    if (!d || !out) fail(XE_ERR_ARG, "null argument");
+    if (d->D <= 0 || d->T <= 0 || d->E < 0) fail(XE_ERR_DIMENSION_MISMATCH, "bad dimensions");
+    HostProblem h;
+    h.D = d->D;
+    h.T = d->T;
+    h.E = d->E;
+    for (int i = 0; i < h.D; ++i) h.device_ids.push_back("d" + std::to_string(i));
+    for (int i = 0; i < h.T; ++i) h.op_names.push_back("op" + std::to_string(i));
+    h.mass = vec(d->output_bytes, static_cast<size_t>(h.T));
+    h.cost = vec(d->cost_ms, static_cast<size_t>(h.D) * h.T);
+    h.src = vec(d->edge_src, static_cast<size_t>(h.E));
+    h.dst = vec(d->edge_dst, static_cast<size_t>(h.E));
+    h.w = vec(d->copy_ms, static_cast<size_t>(h.E) * h.D * h.D);
+    h.budget = vec(d->budget_bytes, static_cast<size_t>(h.D));
+    for (int64_t m : h.mass)
+      if (m <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "output_bytes must be positive");
+    for (int64_t b : h.budget)
+      if (b <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "budget_bytes must be positive");
+    for (double c : h.cost)
+      if (c < 0) fail(XE_ERR_NEGATIVE_COST, "cost_ms must be non-negative");
+    for (double c : h.w)
+      if (c < 0) fail(XE_ERR_NEGATIVE_COST, "copy_ms must be non-negative");
+    h.has_energy = d->has_energy != 0;
+    h.q.assign(static_cast<size_t>(h.D) * h.T, 0.0);
+    h.has_lim.assign(static_cast<size_t>(h.D), 0);
+    h.lim.assign(static_cast<size_t>(h.D), 0.0);
+    if (h.has_energy) {
+      h.alpha = d->alpha;
+      h.q = vec(d->q_joules, static_cast<size_t>(h.D) * h.T);
+      if (d->has_dev_limit) h.has_lim = vec(d->has_dev_limit, static_cast<size_t>(h.D));
+      if (d->dev_limit) h.lim = vec(d->dev_limit, static_cast<size_t>(h.D));
+      h.has_total = d->has_total_limit != 0;
+      h.total_limit = d->total_limit;
+      h.board = d->board_joules;
+    }
+    validate(h);
+    *out = make_handle(std::move(h), device);
+  });
+}
+
+int xe_problem_destroy(xe_problem* p) {
+  return guard([&] {
+    if (!p) return;
+    if (p->device >= 0) {
+      cudaSetDevice(p->device);
+      if (p->stream) cudaStreamDestroy(p->stream);
+    }
+    delete p;
+  });
+}
+
+int xe_problem_describe(const xe_problem* p, xe_problem_desc* o) {
+  return guard([&] {
+    if (!p || !o) fail(XE_ERR_ARG, "null argument");
+    const HostProblem& h = p->h;
+    std::memset(o, 0, sizeof *o);
+    o->D = h.D;
+    o->T = h.T;
+    o->E = h.E;
+    o->output_bytes = h.mass.data();
+    o->cost_ms = h.cost.data();
+    o->edge_src = h.src.data();
+    o->edge_dst = h.dst.data();
+    o->copy_ms = h.w.data();
+    o->budget_bytes = h.budget.data();
+    o->has_energy = h.has_energy;
+    o->alpha = h.alpha;
+    o->q_joules = h.q.data();
+    o->has_dev_limit = h.has_lim.data();
+    o->dev_limit = h.lim.data();
+    o->has_total_limit = h.has_total;
+    o->total_limit = h.total_limit;
+    o->board_joules = h.board;
+  });
+}
+
+int xe_problem_with_budgets(const xe_problem* p, const int64_t* budgets, xe_problem** out) {
+  return guard([&] {
+    if (!p || !budgets || !out) fail(XE_ERR_ARG, "null argument");
+    HostProblem h = p->h;
+    require_uploaded(p);
+    for (int d = 0; d < h.D; ++d) {
+      if (budgets[d] <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "budget for device " + h.device_ids[static_cast<size_t>(d)]);
+      h.budget[static_cast<size_t>(d)] = budgets[d];
+    }
+    *out = make_handle(std::move(h), p->device);
+  });
+}
+
+int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes, int64_t n,
+                  xe_eval_out* out, uint32_t valid_mask, xe_best* best, void* stream) {
+  return guard([&] {
+    if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    xe_model_opts o = opts_or_default(opts);
+    auto* mp = const_cast<xe_problem*>(p);
+    uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
+    eval_cubes_device(p, o, cubes, n, out ? out->obj : nullptr, out ? out->peak : nullptr,
+                      out ? out->flags : nullptr, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+    if (best) read_best(best3, s, best);
+  });
+}
+
+// End-to-end path: host candidates in, host results out.  Chunks are
+// pipelined over two streams so the host->device copy of chunk k+1 overlaps
+// the evaluation of chunk k.
+int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
+                       int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best) {
+  return guard([&] {
+    if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    xe_model_opts o = opts_or_default(opts);
+    const HostProblem& h = p->h;
+    const size_t cb = xe_cube_bytes(h.D, h.T);
+    const int64_t chunk = std::max<int64_t>(1024, static_cast<int64_t>((256ull << 20) / cb));
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    cudaStream_t st[2];
+    XE_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+    XE_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+    struct Bufs {
+      DevBuf<uint32_t> cubes;
+      DevBuf<double> obj;
+      DevBuf<int64_t> peak;
+      DevBuf<uint32_t> flags;
+      DevBuf<unsigned char> scratch;
+    } b[2];
+    const size_t sb = eval_scratch_bytes(p->device);
+    for (int k = 0; k < 2; ++k) {
+      b[k].cubes.alloc(static_cast<size_t>(std::min(chunk, std::max<int64_t>(n, 1))) * cb / 4);
+      if (out && out->obj) b[k].obj.alloc(static_cast<size_t>(chunk));
+      if (out && out->peak) b[k].peak.alloc(static_cast<size_t>(chunk) * h.D);
+      if (out && out->flags) b[k].flags.alloc(static_cast<size_t>(chunk));
+      b[k].scratch.alloc(sb);
+    }
+    DevBuf<uint64_t> best_all;
+    best_all.alloc(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+    try {
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int k = static_cast<int>(c & 1);
+        const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+        XE_CUDA(cudaMemcpyAsync(b[k].cubes.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb,
+                                static_cast<size_t>(m) * cb, cudaMemcpyHostToDevice, st[k]));
+        eval_cubes_device(p, o, b[k].cubes.p, m, b[k].obj.p, b[k].peak.p, b[k].flags.p, valid_mask,
+                          best_all.p + 3 * c, b[k].scratch.p, st[k]);
+        if (out && out->obj)
+          XE_CUDA(cudaMemcpyAsync(out->obj + lo, b[k].obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st[k]));
+        if (out && out->peak)
+          XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, b[k].peak.p, m * h.D * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, st[k]));
+        if (out && out->flags)
+          XE_CUDA(cudaMemcpyAsync(out->flags + lo, b[k].flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, st[k]));
+      }
+      XE_CUDA(cudaStreamSynchronize(st[0]));
+      XE_CUDA(cudaStreamSynchronize(st[1]));
+      if (best) {
+        std::vector<uint64_t> hb(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+        if (nchunks) XE_CUDA(cudaMemcpy(hb.data(), best_all.p, hb.size() * 8, cudaMemcpyDeviceToHost));
+        best->index = -1;
+        best->n_valid = 0;
+        best->obj = INFINITY;
+        uint64_t bk = ~0ull;
+        for (int64_t c = 0; c < nchunks; ++c) {
+          const int64_t idx = static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 1)]);
+          best->n_valid += static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 2)]);
+          if (idx >= 0 && hb[static_cast<size_t>(3 * c)] < bk) {  // chunks ascend in index: strict <
+            bk = hb[static_cast<size_t>(3 * c)];
+            best->index = c * chunk + idx;
+            std::memcpy(&best->obj, &bk, 8);
+          }
+        }
+      }
+    } catch (...) {
+      cudaStreamSynchronize(st[0]);
+      cudaStreamSynchronize(st[1]);
+      cudaStreamDestroy(st[0]);
+      cudaStreamDestroy(st[1]);
+      throw;
+    }
+    cudaStreamDestroy(st[0]);
+    cudaStreamDestroy(st[1]);
+  });
+}
+
+}  // extern "C"

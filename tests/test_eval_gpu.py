@@ -1,0 +1,103 @@
+# SPDX-License-Identifier: Apache-2.0
+"""K2a parity on the GPU: the sm_100a evaluator against the reference's
+golden vectors (bit-exact objective bits, peaks, flags) and against the CPU
+oracle on fresh seeded candidates for every config shape."""
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, golden_npz, golden_problem_text
+from oracle import xo
+from bench import configs
+import cubegen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2212_09290_b200 as xe  # noqa: E402
+from paper_2212_09290_b200 import _lib  # noqa: E402
+
+
+def doc(name):
+    if name in FIXTURES:
+        return golden_problem_text(name)
+    if name.startswith("rand"):
+        return configs.random_small_doc(int(name[4:]), D=3)
+    return configs.CONFIGS[name]()
+
+
+def run_gpu(problem, cubes, strict=False, energy=False):
+    t = torch.from_numpy(np.ascontiguousarray(cubes).view(np.int32)).cuda()
+    r = xe.evaluate_cubes(problem, t, xe.ModelOptions(strict_free=strict, energy=energy))
+    torch.cuda.synchronize()
+    return (r.obj.cpu().numpy(), r.peak.cpu().numpy(), r.flags.cpu().numpy().view(np.uint32), r)
+
+
+def compare(o, p, f, ro, rp, rf):
+    assert np.array_equal(o.view(np.int64), ro.view(np.int64)), \
+        f"objective bits differ at {np.nonzero(o.view(np.int64) != ro.view(np.int64))[0][:5]}"
+    assert np.array_equal(p, rp), f"peaks differ at {np.nonzero((p != rp).any(1))[0][:5]}"
+    mask = 0xFFFF | _lib.F_DECODE
+    bad = np.nonzero((f & mask) != (rf & mask))[0]
+    assert len(bad) == 0, f"flags differ at {bad[:5]}: {[hex(f[i]) for i in bad[:5]]} vs {[hex(rf[i]) for i in bad[:5]]}"
+    comparable = ((rf & _lib.F_DECODE) != 0) & ((f & _lib.F_EQ12) == 0)
+    assert np.array_equal((f & _lib.F_DECODE_FREED)[comparable], (rf & _lib.F_DECODE_FREED)[comparable])
+
+
+@pytest.mark.parametrize("name", FIXTURES + ["vgg16", "rand3", "rand7", "rand11"])
+def test_eval_vs_reference_golden(name):
+    z = golden_npz("eval_" + name)
+    prob = xe.Problem.from_json(doc(name))
+    for strict in (0, 1):
+        for en in ((0, 1) if name == "fig2_energy" else (0,)):
+            o, p, f, _ = run_gpu(prob, z["cubes"], strict, en)
+            compare(o, p, f, z[f"obj_s{strict}e{en}"], z[f"peak_s{strict}e{en}"], z[f"flags_s{strict}e{en}"])
+
+
+@pytest.mark.parametrize("name,n", [("fig2", 3000), ("vgg16", 400), ("resnet50", 40), ("unet", 30),
+                                    ("rand3", 2000)])
+def test_eval_vs_oracle_fresh(oracle, name, n):
+    text = doc(name)
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    cubes = cubegen.mixed_cubes(a, n, seed=99, random_frac=0.02)
+    for strict in (0, 1):
+        o, p, f, _ = run_gpu(prob, cubes, strict)
+        ro, rp, rf = oracle.eval_cubes(a, cubes, strict)
+        compare(o, p, f, ro, rp, rf)
+
+
+def test_best_of_batch_and_host_path(oracle):
+    text = doc("vgg16")
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    cubes = cubegen.mixed_cubes(a, 2000, seed=5, random_frac=0.0)
+    o, p, f, r = run_gpu(prob, cubes)
+    valid = (f & _lib.F_CHECK_MASK) == 0
+    assert r.n_valid == int(valid.sum()) > 0
+    idx = np.nonzero(valid)[0]
+    best = idx[np.argmin(o[idx])]          # first minimum (solver.cpp:57-61 rule)
+    assert r.best_index == best and r.best_obj == o[best]
+    h = xe.evaluate_cubes_host(prob, cubes)
+    assert np.array_equal(h.obj.view(np.int64), o.view(np.int64))
+    assert np.array_equal(h.peak, p) and np.array_equal(h.flags, f)
+    assert h.best_index == r.best_index and h.n_valid == r.n_valid
+    # budget-aware validity: the integer budget bit joins the mask
+    r2 = xe.evaluate_cubes(prob, torch.from_numpy(cubes.view(np.int32)).cuda(),
+                           valid_mask=_lib.F_CHECK_MASK | _lib.F_BUDGET)
+    v2 = valid & ((f & _lib.F_BUDGET) == 0)
+    assert r2.n_valid == int(v2.sum())
+
+
+def test_unaligned_and_odd_sizes(oracle):
+    # chain3: 24-byte cubes (no bulk copy); odd candidate counts; n = 0
+    text = doc("chain3")
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    for n in (1, 15, 17, 33, 1000):
+        cubes = cubegen.mixed_cubes(a, n, seed=n)
+        o, p, f, _ = run_gpu(prob, cubes)
+        ro, rp, rf = oracle.eval_cubes(a, cubes)
+        compare(o, p, f, ro, rp, rf)
+    t = torch.zeros((0, prob.cube_words), dtype=torch.int32, device="cuda")
+    r = xe.evaluate_cubes(prob, t)
+    assert r.best_index == -1 and r.n_valid == 0
