@@ -154,22 +154,44 @@ def _ptr(t):
 
 
 def evaluate_cubes(problem: Problem, cubes, opts: Optional[ModelOptions] = None,
-                   valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True, stream=None):
+                   valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True, stream=None,
+                   out=None, best: bool = True):
     """Evaluate device-resident cubes (torch uint32/int32 CUDA tensor of
-    shape [n, cube_words]).  Returns EvalResult with torch tensors."""
+    shape [n, cube_words]).  Returns EvalResult with torch tensors.
+    out=(obj, peak, flags) reuses preallocated device tensors; best=False
+    skips the best-of-batch reduction and its host read (asynchronous)."""
     import torch
     opts = opts or ModelOptions()
     n = cubes.shape[0] if cubes.dim() > 1 else cubes.numel() // problem.cube_words
     dev = cubes.device
-    obj = torch.empty(n, dtype=torch.float64, device=dev) if outputs else None
-    peak = torch.empty((n, problem.D), dtype=torch.int64, device=dev) if outputs else None
-    flags = torch.empty(n, dtype=torch.int32, device=dev) if outputs else None
-    out = _lib.EvalOut(_ptr(obj), _ptr(peak), _ptr(flags))
-    best = _lib.Best()
+    if out is not None:
+        obj, peak, flags = out
+    else:
+        obj = torch.empty(n, dtype=torch.float64, device=dev) if outputs else None
+        peak = torch.empty((n, problem.D), dtype=torch.int64, device=dev) if outputs else None
+        flags = torch.empty(n, dtype=torch.int32, device=dev) if outputs else None
+    eo = _lib.EvalOut(_ptr(obj), _ptr(peak), _ptr(flags))
+    b = _lib.Best()
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     check(LIB.xe_eval_cubes(problem.handle, C.byref(opts.c()), C.c_void_p(cubes.data_ptr()), n,
-                            C.byref(out), valid_mask, C.byref(best), C.c_void_p(s)))
-    return EvalResult(obj, peak, flags, best.obj, best.index, best.n_valid)
+                            C.byref(eo), valid_mask, C.byref(b) if best else None, C.c_void_p(s)))
+    if not best:
+        return EvalResult(obj, peak, flags, float("nan"), -1, -1)
+    return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
+
+
+def round_cubes(problem: Problem, n: int, seed: int, first: int = 0, edits: int = 3,
+                perturb: float = 0.1, x=None, out=None, stream=None):
+    """K4: n candidate cubes (torch int32 CUDA tensor [n, cube_words]) sampled
+    from LP marginals x (device float64 tensor over the model's columns) or
+    uniformly when x is None; candidate k is a pure function of (seed, first+k)."""
+    import torch
+    if out is None:
+        out = torch.empty((n, problem.cube_words), dtype=torch.int32, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.xe_round_cubes(problem.handle, _ptr(x), seed, first, n, edits, perturb,
+                             C.c_void_p(out.data_ptr()), C.c_void_p(s)))
+    return out
 
 
 def evaluate_cubes_host(problem: Problem, cubes: np.ndarray, opts: Optional[ModelOptions] = None,

@@ -22,6 +22,8 @@ size_t eval_scratch_bytes(int device);
 void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const uint32_t* cubes,
                        int64_t n, double* obj, int64_t* peak, uint32_t* flags, uint32_t valid_mask,
                        uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
+void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
+                        int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s);
 
 namespace {
 
@@ -293,6 +295,16 @@ int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uin
     }
     cudaStreamDestroy(st[0]);
     cudaStreamDestroy(st[1]);
+  });
+}
+
+int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int64_t first,
+                   int64_t n, int32_t edits, double perturb, uint32_t* cubes_dev, void* stream) {
+  return guard([&] {
+    if (!p || (!cubes_dev && n > 0) || n < 0 || edits < 0) fail(XE_ERR_ARG, "bad argument");
+    require_uploaded(p);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    round_cubes_device(p, x_dev, seed, first, n, edits, perturb, cubes_dev, s);
   });
 }
 

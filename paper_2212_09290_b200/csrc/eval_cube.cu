@@ -121,17 +121,20 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
     x = align16(x + kSlots * (8 + 4 + 4) + 8 * kSlots * P.D);
     return x;
   };
-  while (!exact && cap > 16 && a.off_warp + kWarps * warp_total(cap) > smem_limit) cap /= 2;
+  int warps = kWarps;
+  while (warps > 1 && a.off_warp + warps * warp_total(cap) > smem_limit) --warps;
+  while (!exact && cap > 16 && a.off_warp + warps * warp_total(cap) > smem_limit) cap /= 2;
+  a.warps = warps;
   a.cap = cap;
   a.off_w_slot = align16(a.off_w_terms + 2 * kSlots * cap);
   a.warp_bytes = warp_total(cap);
-  const int smem = a.off_warp + kWarps * a.warp_bytes;
+  const int smem = a.off_warp + warps * a.warp_bytes;
   if (smem > smem_limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the shared-memory plan");
 
   int nsm = 0;
   XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
   const int64_t nblocks = (n + kSlots - 1) / kSlots;
-  const int grid_cap = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nblocks + kWarps - 1) / kWarps, static_cast<int64_t>(nsm) * 8)));
+  const int grid_cap = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nblocks + warps - 1) / warps, static_cast<int64_t>(nsm) * 8)));
 
   const size_t nw_max = static_cast<size_t>(nsm) * 8 * kWarps;
   unsigned char* sc = scratch;
@@ -148,7 +151,7 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
       default: grid = launch_nw4(a, grid_cap, smem, stream, nsm); break;
     }
   }
-  const size_t nw = static_cast<size_t>(grid) * kWarps;
+  const size_t nw = static_cast<size_t>(grid) * warps;
   if (best3) {
     if (n > 0) {
       reduce_best_kernel<<<1, 256, 0, stream>>>(a.wbest_key, a.wbest_idx, a.wvalid, static_cast<int>(nw),

@@ -57,6 +57,7 @@ struct EvalArgs {
       off_ebad, off_q, off_warp;
   int warp_bytes, off_w_stage, off_w_bar, off_w_terms, off_w_slot;
   int stages, cap, use_bulk;
+  int warps;  // warps per CTA (shared-memory plan decides, <= kWarps)
   uint32_t cube_words;
 };
 
@@ -287,8 +288,8 @@ __global__ void __launch_bounds__(kWarps * 32) eval_cube_kernel(const EvalArgs a
   fence_mbar_init();
   __syncthreads();
 
-  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * a.warps + wid;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * a.warps;
   const int64_t nblocks = (a.n + kSlots - 1) / kSlots;
   const uint32_t cube_bytes = a.cube_words * 4u;
 
@@ -672,10 +673,10 @@ int launch_t(const EvalArgs& a, int grid_cap, int smem, cudaStream_t s, int nsm)
   auto k = eval_cube_kernel<NW, MAXD, EXACT>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
-  XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarps * 32, smem));
+  XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, a.warps * 32, smem));
   if (per_sm < 1) fail(XE_ERR_TOO_LARGE, "evaluator does not fit on an SM");
   int grid = std::max(1, std::min(grid_cap, nsm * per_sm));  // persistent: one wave
-  k<<<grid, kWarps * 32, smem, s>>>(a);
+  k<<<grid, a.warps * 32, smem, s>>>(a);
   XE_CUDA(cudaGetLastError());
   return grid;
 }

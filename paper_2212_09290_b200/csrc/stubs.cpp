@@ -19,5 +19,4 @@ int xe_csr_last_build_ms(const xe_csr*, float*) { XE_TODO("xe_csr_last_build_ms"
 int xe_eval_placements(const xe_problem*, const uint8_t*, int64_t, int32_t, xe_eval_out*, uint32_t, xe_best*, void*) { XE_TODO("xe_eval_placements"); }
 int xe_assignment_oracle(const xe_problem*, double*, int32_t*, int64_t*) { XE_TODO("xe_assignment_oracle"); }
 int xe_pdhg_solve(xe_csr*, const xe_pdhg_opts*, xe_pdhg_result*, double*, double*) { XE_TODO("xe_pdhg_solve"); }
-int xe_round_cubes(const xe_problem*, const double*, uint64_t, int64_t, int64_t, int32_t, double, uint32_t*, void*) { XE_TODO("xe_round_cubes"); }
 }
