@@ -206,8 +206,8 @@ typedef struct xe_best {
 
 /* Evaluates n candidates.  cubes, out arrays: device pointers.  out may have
  * NULL members to skip writing them.  best (host, may be NULL) receives the
- * argmin over candidates whose flags & valid_mask == 0.  stream = 0 -> the
- * handle's stream. */
+ * argmin over candidates whose flags & valid_mask == 0.  stream: a cudaStream_t;
+ * NULL is the legacy default stream (as in every CUDA library). */
 int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                   int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best,
                   void* stream);

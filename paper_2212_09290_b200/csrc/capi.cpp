@@ -5,6 +5,7 @@
 // xe::guard.  There is no CPU fallback: without a CUDA device every compute
 // entry point returns XE_ERR_NO_DEVICE.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -67,6 +68,30 @@ namespace {
 xe_model_opts opts_or_default(const xe_model_opts* o) {
   xe_model_opts d{};
   return o ? *o : d;
+}
+
+// Host->device copy through the driver API: page-locked buffers allocated by
+// another CUDA runtime instance in the process (e.g. torch's pinned memory)
+// are recognised by the driver and DMA'd directly; cudart's own tracking
+// only knows its own allocations.
+// (The entry point is fetched from the runtime, so the library does not
+// link libcuda and still loads on GPU-less hosts.)
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  using Fn = CUresult (*)(CUdeviceptr, const void*, size_t, CUstream);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemcpyHtoDAsync", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) {
+    XE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  CUresult r = fn(reinterpret_cast<CUdeviceptr>(dst), src, bytes, reinterpret_cast<CUstream>(s));
+  if (r != CUDA_SUCCESS) fail(XE_ERR_CUDA, "cuMemcpyHtoDAsync failed: " + std::to_string(static_cast<int>(r)));
 }
 
 void read_best(const uint64_t* dev3, cudaStream_t s, xe_best* best) {
@@ -208,7 +233,7 @@ int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t
   return guard([&] {
     if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
     require_uploaded(p);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     xe_model_opts o = opts_or_default(opts);
     auto* mp = const_cast<xe_problem*>(p);
     uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
@@ -255,8 +280,8 @@ int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uin
       for (int64_t c = 0; c < nchunks; ++c) {
         const int k = static_cast<int>(c & 1);
         const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
-        XE_CUDA(cudaMemcpyAsync(b[k].cubes.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb,
-                                static_cast<size_t>(m) * cb, cudaMemcpyHostToDevice, st[k]));
+        h2d(b[k].cubes.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
+            st[k]);
         eval_cubes_device(p, o, b[k].cubes.p, m, b[k].obj.p, b[k].peak.p, b[k].flags.p, valid_mask,
                           best_all.p + 3 * c, b[k].scratch.p, st[k]);
         if (out && out->obj)
@@ -303,7 +328,7 @@ int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int6
   return guard([&] {
     if (!p || (!cubes_dev && n > 0) || n < 0 || edits < 0) fail(XE_ERR_ARG, "bad argument");
     require_uploaded(p);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     round_cubes_device(p, x_dev, seed, first, n, edits, perturb, cubes_dev, s);
   });
 }

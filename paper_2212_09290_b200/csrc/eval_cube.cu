@@ -107,27 +107,38 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
   // serial term-list capacity: covers placements plus a few recomputes and
   // copies; larger candidates take the (slow, exact) one-lane path
   int cap = exact ? 0 : ((std::min(1024, 2 * P.T + 32) + 7) & ~7);
-  // per-warp: stages | barriers | term lists | slot results
+  int cap2 = (exact || !a.energy) ? 0 : cap;
+  // per-warp: stages | barriers | term lists (R+copy) | energy terms | slot results
   int w = 0;
   a.off_w_stage = w;
   w = align16(w + a.stages * cube_bytes);
   a.off_w_bar = w;
   w = align16(w + 8 * a.stages);
   a.off_w_terms = w;
-  int smem_limit = 0;
+  int smem_limit = 0, smem_sm = 0;
   XE_CUDA(cudaDeviceGetAttribute(&smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
-  auto warp_total = [&](int c) {
+  XE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, pr->device));
+  auto warp_total = [&](int c, int c2) {
     int x = align16(a.off_w_terms + 2 * kSlots * c);
-    x = align16(x + kSlots * (8 + 4 + 4) + 8 * kSlots * P.D);
+    x = align16(x + 2 * kSlots * c2);
+    x = align16(x + kSlots * (8 + 4 + 4 + 4) + 8 * kSlots * P.D);
     return x;
   };
+  // prefer two resident CTAs per SM (occupancy), else the most warps that fit
   int warps = kWarps;
-  while (warps > 1 && a.off_warp + warps * warp_total(cap) > smem_limit) --warps;
-  while (!exact && cap > 16 && a.off_warp + warps * warp_total(cap) > smem_limit) cap /= 2;
+  const int two = smem_sm / 2 - 1024;
+  while (warps > 4 && a.off_warp + warps * warp_total(cap, cap2) > two) --warps;
+  while (warps > 1 && a.off_warp + warps * warp_total(cap, cap2) > smem_limit) --warps;
+  while (!exact && cap > 16 && a.off_warp + warps * warp_total(cap, cap2) > smem_limit) {
+    cap /= 2;
+    cap2 = cap2 ? cap : 0;
+  }
   a.warps = warps;
   a.cap = cap;
-  a.off_w_slot = align16(a.off_w_terms + 2 * kSlots * cap);
-  a.warp_bytes = warp_total(cap);
+  a.cap2 = cap2;
+  a.off_w_terms2 = align16(a.off_w_terms + 2 * kSlots * cap);
+  a.off_w_slot = align16(a.off_w_terms2 + 2 * kSlots * cap2);
+  a.warp_bytes = warp_total(cap, cap2);
   const int smem = a.off_warp + warps * a.warp_bytes;
   if (smem > smem_limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the shared-memory plan");
 

@@ -156,9 +156,19 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
         int pc = rng.below(n_c), t = -1;
         for (int e = 0; e < a.E; ++e)
           if (a.src[e] == i && a.dst[e] > i + 1 && pc-- == 0) t = a.dst[e];
+        // the drop window must not cover a timestep where i is needed: any
+        // earlier computation (diagonal or recomputed) of a consumer of i
         int a0 = i + 1;
-        for (int e = 0; e < a.E; ++e)
-          if (a.src[e] == i && a.dst[e] < t && a.dst[e] + 1 > a0) a0 = a.dst[e] + 1;
+        for (int tt = t - 1; tt > i && a0 == i + 1; --tt)
+          for (int e = 0; e < a.E; ++e) {
+            if (a.src[e] != i) continue;
+            bool used = false;
+            for (int d = 0; d < D; ++d) used |= bit_get(0, d, tt, a.dst[e]);
+            if (used) {
+              a0 = tt + 1;
+              break;
+            }
+          }
         if (a0 > t) continue;
         const int a1 = a0 + rng.below(t - a0 + 1);
         const int di = dev[i];
