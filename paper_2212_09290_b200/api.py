@@ -180,6 +180,95 @@ def evaluate_cubes(problem: Problem, cubes, opts: Optional[ModelOptions] = None,
     return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
 
 
+class _DevArray:
+    """__cuda_array_interface__ view of a device pointer owned by the library."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr or 0), True), "version": 3}
+
+
+def _dev_tensor(ptr, n, typestr):
+    import torch
+    return torch.as_tensor(_DevArray(ptr, n, typestr), device="cuda")
+
+
+TAGS = ["EQ7", "EQ8", "EQ9", "EQ10", "EQ11", "EQ12", "EQ13", "EQ14", "EQ16_LO", "EQ16_HI",
+        "Z_LINK", "P_LINK", "ENERGY_DEV", "ENERGY_TOTAL"]
+
+
+class Model:
+    """Device-resident MILP (xe_csr): the B200 counterpart of MilpModel
+    (model.hpp:81-101) as CSR over closed-form VarRef columns."""
+
+    def __init__(self, problem: "Problem", handle):
+        self.problem = problem
+        self._h = handle
+        info = _lib.CsrInfo()
+        check(LIB.xe_csr_get_info(self._h, C.byref(info)))
+        self.n_cols, self.n_rows, self.nnz = info.n_cols, info.n_rows, info.nnz
+        self.tag_rows = {TAGS[i]: info.tag_rows[i] for i in range(14)}
+        v = _lib.CsrView()
+        check(LIB.xe_csr_get_view(self._h, C.byref(v)))
+        self._v = v
+
+    def __del__(self):
+        try:
+            if self._h:
+                LIB.xe_csr_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def build_ms(self) -> float:
+        ms = C.c_float()
+        check(LIB.xe_csr_last_build_ms(self._h, C.byref(ms)))
+        return ms.value
+
+    def device_arrays(self) -> dict:
+        """Zero-copy torch views of the device model."""
+        v, m, n, z = self._v, self.n_rows, self.n_cols, self.nnz
+        return {
+            "row_ptr": _dev_tensor(v.row_ptr, m + 1, "<i8"), "col": _dev_tensor(v.col, z, "<i4"),
+            "val": _dev_tensor(v.val, z, "<f8"), "rhs": _dev_tensor(v.rhs, m, "<f8"),
+            "sense": _dev_tensor(v.sense, m, "|i1"), "tag": _dev_tensor(v.tag, m, "|u1"),
+            "ordinal": _dev_tensor(v.ordinal, m, "<i4"), "obj": _dev_tensor(v.obj, n, "<f8"),
+            "obj_present": _dev_tensor(v.obj_present, n, "|u1"), "lb": _dev_tensor(v.lb, n, "<f8"),
+            "ub": _dev_tensor(v.ub, n, "<f8"), "kind": _dev_tensor(v.kind, n, "|u1"),
+        }
+
+    def to_host(self) -> dict:
+        return {k: t.cpu().numpy() for k, t in self.device_arrays().items()}
+
+    def csc(self) -> dict:
+        check(LIB.xe_csr_build_csc(self._h))
+        cp, r, val = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(LIB.xe_csr_get_csc(self._h, C.byref(cp), C.byref(r), C.byref(val)))
+        return {"col_ptr": _dev_tensor(cp.value, self.n_cols + 1, "<i8"),
+                "row": _dev_tensor(r.value, self.nnz, "<i4"),
+                "val": _dev_tensor(val.value, self.nnz, "<f8")}
+
+    def write_mps(self) -> bytes:
+        """write_mps (mps_io.cpp:109-199), byte-identical."""
+        n = C.c_size_t()
+        check(LIB.xe_write_mps(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(LIB.xe_write_mps(self._h, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+
+def build_model(problem: "Problem", opts: Optional[ModelOptions] = None) -> Model:
+    """build_model (model.cpp:86-256) on the GPU (K1)."""
+    opts = opts or ModelOptions()
+    h = C.c_void_p()
+    check(LIB.xe_build_csr(problem.handle, C.byref(opts.c()), C.byref(h)))
+    return Model(problem, h)
+
+
 def round_cubes(problem: Problem, n: int, seed: int, first: int = 0, edits: int = 3,
                 perturb: float = 0.1, x=None, out=None, stream=None):
     """K4: n candidate cubes (torch int32 CUDA tensor [n, cube_words]) sampled

@@ -8,14 +8,6 @@ using namespace xe;
 #define XE_TODO(name) set_last_error(std::string(name) + ": not implemented in this build"); return XE_ERR_ARG
 
 extern "C" {
-int xe_build_csr(const xe_problem*, const xe_model_opts*, xe_csr**) { XE_TODO("xe_build_csr"); }
-int xe_csr_destroy(xe_csr*) { return XE_OK; }
-int xe_csr_get_info(const xe_csr*, xe_csr_info*) { XE_TODO("xe_csr_get_info"); }
-int xe_csr_get_view(const xe_csr*, xe_csr_view*) { XE_TODO("xe_csr_get_view"); }
-int xe_csr_build_csc(xe_csr*) { XE_TODO("xe_csr_build_csc"); }
-int xe_csr_get_csc(const xe_csr*, const int64_t**, const int32_t**, const double**) { XE_TODO("xe_csr_get_csc"); }
-int xe_write_mps(xe_csr*, char*, size_t*) { XE_TODO("xe_write_mps"); }
-int xe_csr_last_build_ms(const xe_csr*, float*) { XE_TODO("xe_csr_last_build_ms"); }
 int xe_eval_placements(const xe_problem*, const uint8_t*, int64_t, int32_t, xe_eval_out*, uint32_t, xe_best*, void*) { XE_TODO("xe_eval_placements"); }
 int xe_assignment_oracle(const xe_problem*, double*, int32_t*, int64_t*) { XE_TODO("xe_assignment_oracle"); }
 int xe_pdhg_solve(xe_csr*, const xe_pdhg_opts*, xe_pdhg_result*, double*, double*) { XE_TODO("xe_pdhg_solve"); }

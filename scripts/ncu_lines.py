@@ -12,8 +12,8 @@ from collections import defaultdict
 rep, cubin, sym = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 syms = subprocess.run(["cuobjdump", "-symbols", cubin], capture_output=True, text=True).stdout
-name = [l.split()[-1] for l in syms.splitlines() if sym in l][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+name = [l.split()[-1] for l in syms.splitlines() if sym in l and "$" not in l.split()[-1] and l.split()[0] == "STT_FUNC"][0]
+dis = subprocess.run(["nvdisasm", "-gi", "-c", cubin], capture_output=True, text=True).stdout
 addr2line, cur, inside = {}, None, False
 for l in dis.splitlines():
     if l.startswith(".text."):
@@ -21,9 +21,11 @@ for l in dis.splitlines():
         continue
     if not inside:
         continue
-    m = re.search(r'//## File "([^"]+)", line (\d+)', l)
-    if m:
-        cur = f"{m.group(1).split('/')[-1]}:{m.group(2)}"
+    if "//## File" in l:
+        locs = re.findall(r'"([^"]+)", line (\d+)', l)
+        # outermost call site (last in the inlining chain) unless --inner
+        f, n = locs[0] if "--inner" in sys.argv else locs[-1]
+        cur = f"{f.split('/')[-1]}:{n}"
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
     if m and cur:
