@@ -185,7 +185,7 @@ class _DevArray:
 
     def __init__(self, ptr, n, typestr):
         self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
-                                         "data": (int(ptr or 0), True), "version": 3}
+                                         "data": (int(ptr or 0), False), "version": 3}
 
 
 def _dev_tensor(ptr, n, typestr):
@@ -259,6 +259,39 @@ class Model:
         buf = C.create_string_buffer(n.value)
         check(LIB.xe_write_mps(self._h, buf, C.byref(n)))
         return buf.raw[: n.value]
+
+
+@dataclass
+class LpResult:
+    primal_obj: float
+    dual_obj: float
+    rel_gap: float
+    rel_primal_res: float
+    iters: int
+    restarts: int
+    converged: bool
+    solve_ms: float
+    ms_per_iter: float
+    x: Optional[np.ndarray] = None
+    y: Optional[np.ndarray] = None
+
+
+def pdhg_solve(model: Model, tol: float = 1e-6, max_iters: int = 200000, check_every: int = 64,
+               lb=None, ub=None, return_x: bool = False, return_y: bool = False,
+               verbose: bool = False) -> LpResult:
+    """K3: LP relaxation of the model by PDHG (restarted, preconditioned).
+    lb/ub: optional per-column bound overrides (branch-and-bound nodes)."""
+    lbo = None if lb is None else np.ascontiguousarray(lb, np.float64)
+    ubo = None if ub is None else np.ascontiguousarray(ub, np.float64)
+    o = _lib.PdhgOpts(max_iters, tol, check_every, int(verbose),
+                      None if lbo is None else lbo.ctypes.data, None if ubo is None else ubo.ctypes.data)
+    r = _lib.PdhgResult()
+    x = np.empty(model.n_cols) if return_x else None
+    y = np.empty(model.n_rows) if return_y else None
+    check(LIB.xe_pdhg_solve(model.handle, C.byref(o), C.byref(r),
+                            None if x is None else x.ctypes.data, None if y is None else y.ctypes.data))
+    return LpResult(r.primal_obj, r.dual_obj, r.rel_gap, r.rel_primal_res, r.iters, r.restarts,
+                    r.status == 0, r.solve_ms, r.spmv_ms_per_iter, x, y)
 
 
 def build_model(problem: "Problem", opts: Optional[ModelOptions] = None) -> Model:

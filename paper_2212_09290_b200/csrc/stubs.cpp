@@ -10,5 +10,4 @@ using namespace xe;
 extern "C" {
 int xe_eval_placements(const xe_problem*, const uint8_t*, int64_t, int32_t, xe_eval_out*, uint32_t, xe_best*, void*) { XE_TODO("xe_eval_placements"); }
 int xe_assignment_oracle(const xe_problem*, double*, int32_t*, int64_t*) { XE_TODO("xe_assignment_oracle"); }
-int xe_pdhg_solve(xe_csr*, const xe_pdhg_opts*, xe_pdhg_result*, double*, double*) { XE_TODO("xe_pdhg_solve"); }
 }
