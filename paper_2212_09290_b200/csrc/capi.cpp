@@ -25,6 +25,11 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
                        uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
                         int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s);
+void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n, int policy, double* obj,
+                            int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3,
+                            unsigned char* scratch, cudaStream_t s);
+void assignment_oracle_device(const xe_problem* pr, double* best_obj, int32_t* best_dev, int64_t* n_eval,
+                              cudaStream_t s);
 
 namespace {
 
@@ -330,6 +335,28 @@ int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int6
     require_uploaded(p);
     cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     round_cubes_device(p, x_dev, seed, first, n, edits, perturb, cubes_dev, s);
+  });
+}
+
+int xe_eval_placements(const xe_problem* p, const uint8_t* dev, int64_t n, int32_t policy, xe_eval_out* out,
+                       uint32_t valid_mask, xe_best* best, void* stream) {
+  return guard([&] {
+    if (!p || (!dev && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* mp = const_cast<xe_problem*>(p);
+    uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
+    eval_placements_device(p, dev, n, policy, out ? out->obj : nullptr, out ? out->peak : nullptr,
+                           out ? out->flags : nullptr, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+    if (best) read_best(best3, s, best);
+  });
+}
+
+int xe_assignment_oracle(const xe_problem* p, double* best_obj, int32_t* best_dev, int64_t* n_evaluated) {
+  return guard([&] {
+    if (!p || !best_obj || !best_dev || !n_evaluated) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    assignment_oracle_device(p, best_obj, best_dev, n_evaluated, p->stream);
   });
 }
 

@@ -51,6 +51,14 @@ int align16(int x) { return (x + 15) & ~15; }
 
 using namespace cube;
 
+// Lexicographic (objective bits, index) minimum over per-warp partials.
+void reduce_best_launch(const uint64_t* key, const int64_t* idx, const int64_t* valid, int n, uint64_t* out,
+                        cudaStream_t s) {
+  reduce_best_kernel<<<1, 256, 0, s>>>(key, idx, valid, n, out, reinterpret_cast<int64_t*>(out + 1),
+                                       reinterpret_cast<int64_t*>(out + 2));
+  XE_CUDA(cudaGetLastError());
+}
+
 // Host launcher: plans shared memory, launches the evaluator and the
 // best-of-batch reduction into best3 (device: objective bits, index, valid
 // count), all on `stream`, without synchronising.

@@ -1,0 +1,398 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K2b — batched evaluation of device placements, and the assignment oracle.
+//
+// A placement candidate is dev[T] (uint8): op i computed once, at timestep i,
+// on dev[i].  policy 0 is the reference's save-all family
+// (save_all_assignment, proj/src/solver.cpp:30-42): every output stays saved
+// on its device afterwards.  policy 1 (minimal-save) keeps a tensor only
+// until its last consumer and never saves a tensor without consumers.
+// On these cubes the completion has closed forms (verified
+// against complete_assignment/objective_value/check_assignment):
+//   objective = sum_d sum_{t: dev_t = d} c[d][t]              (R terms, d-major)
+//             + sum over edges e=(u->v) in (v, e) order with dev_u != dev_v
+//               of w[e][dev_u][dev_v]                         (copy terms)
+//   save-all peak_d    = sum_{i: dev_i = d} m_i
+//   minimal-save peak_d = max_t ( sum_{u < t <= last(u), dev_u = d} m_u + [dev_t = d] m_t )
+// and only BUDGET / U_BOUND can fail (EQ8/11/12/16 and decode hold).
+//
+// One warp per candidate: the placement is staged in shared memory; lanes
+// stride over ops and edges; EXACT mode sums int64 fixed point (any order),
+// serial mode reproduces objective_value's sequential FP64 order on lane 0.
+//
+// assignment_oracle (solver.cpp:44-75): one thread per odometer index
+// (op 0 most significant), save-all objective in the reference's order,
+// first strict minimum = lowest index among equal objective bits.
+
+#include <climits>
+#include <cstring>
+
+#include "bits.cuh"
+#include "xe_internal.hpp"
+
+namespace xe {
+namespace place {
+
+constexpr int kWarps = 8;
+
+struct Args {
+  int D, T, E, policy, fix_k;
+  const int64_t* mass;
+  const double* cost;     // [D][T]
+  const double* w;        // [E][D][D]
+  const int64_t* tfix;    // [D*T + E*D*D] fixed point
+  const int32_t* src;
+  const int32_t* dst;
+  const int32_t* eorder;  // edges sorted by (dst, e)
+  const int32_t* last;    // last consumer of each op, -1 if none
+  const int32_t* lv_ptr;  // [T+1] ops grouped by last consumer
+  const int32_t* lv_ops;
+  const int64_t* budget;
+  const double* ubound;
+  const uint8_t* dev;
+  int64_t n;
+  double* obj;
+  int64_t* peak;
+  uint32_t* flags;
+  uint32_t valid_mask;
+  uint64_t* wbest_key;
+  int64_t* wbest_idx;
+  int64_t* wvalid;
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kWarps * 32) place_kernel(const Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int T = a.T, D = a.D, E = a.E;
+  const int tb = (T + 15) & ~15;
+  uint8_t* sdev = smem + wid * (tb + 8 * 8 * 2);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+  uint64_t best_key = ~0ull;
+  int64_t best_idx = -1, n_valid = 0;
+
+  for (int64_t c = gw; c < a.n; c += nw) {
+    const uint8_t* g = a.dev + c * T;
+    for (int i = lane; i < T; i += 32) sdev[i] = g[i];
+    __syncwarp();
+    // ---- objective
+    double obj = 0.0;
+    if (EXACT) {
+      int64_t fix = 0;
+      for (int i = lane; i < T; i += 32) fix += a.tfix[sdev[i] * T + i];
+      const int base = D * T;
+      for (int e = lane; e < E; e += 32) {
+        const int du = sdev[a.src[e]], dv = sdev[a.dst[e]];
+        if (du != dv) fix += a.tfix[base + (e * D + du) * D + dv];
+      }
+      fix = warp_sum_i64(fix);
+      obj = ldexp(static_cast<double>(fix), -a.fix_k);
+    } else if (lane == 0) {  // objective_value's order (model.cpp:392-411)
+      double total = 0.0;
+      for (int d = 0; d < D; ++d)
+        for (int t = 0; t < T; ++t)
+          if (sdev[t] == d) total = __dadd_rn(total, a.cost[d * T + t]);
+      for (int k = 0; k < E; ++k) {
+        const int e = a.eorder[k];
+        const int du = sdev[a.src[e]], dv = sdev[a.dst[e]];
+        if (du != dv) total = __dadd_rn(total, a.w[(e * D + du) * D + dv]);
+      }
+      obj = total;
+    }
+    // ---- peaks
+    int64_t pk[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) pk[d] = 0;
+    if (a.policy == 0) {
+      for (int i = lane; i < T; i += 32) {
+        const int d = sdev[i];
+        const int64_t m = a.mass[i];
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (x == d) pk[x] += m;
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (x < D) pk[x] = warp_sum_i64(pk[x]);
+    } else {
+      // exact sequential sweep (lane 0): live sets per device
+      if (lane == 0) {
+        int64_t live[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) live[x] = 0;
+        for (int t = 0; t < T; ++t) {
+          if (t >= 1) {
+            const int u = t - 1;
+            if (a.last[u] >= t) {
+              const int d = sdev[u];
+#pragma unroll
+              for (int x = 0; x < 8; ++x)
+                if (x == d) live[x] += a.mass[u];
+            }
+          }
+          const int dt = sdev[t];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const int64_t v = live[x] + (x == dt ? a.mass[t] : 0);
+            pk[x] = max(pk[x], v);
+          }
+          // tensors whose last consumer is t are not saved into t+1
+          for (int k = a.lv_ptr[t]; k < a.lv_ptr[t + 1]; ++k) {
+            const int u = a.lv_ops[k];
+            if (u >= t) continue;
+            const int d = sdev[u];
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+              if (x == d) live[x] -= a.mass[u];
+          }
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) pk[x] = __shfl_sync(0xffffffffu, pk[x], 0);
+    }
+    obj = __shfl_sync(0xffffffffu, obj, 0);
+    uint32_t fl = 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      if (x >= D) continue;
+      if (pk[x] > a.budget[x]) fl |= XE_F_BUDGET;
+      if (static_cast<double>(pk[x]) > a.ubound[x]) fl |= XE_F_U_BOUND;
+    }
+    if (lane == 0) {
+      if (a.obj) a.obj[c] = obj;
+      if (a.flags) a.flags[c] = fl;
+      if (a.peak)
+        for (int x = 0; x < D; ++x) a.peak[c * D + x] = pk[x];
+      if ((fl & a.valid_mask) == 0) {
+        ++n_valid;
+        const uint64_t key = __double_as_longlong(obj);
+        if (key < best_key || (key == best_key && c < best_idx)) {
+          best_key = key;
+          best_idx = c;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    a.wbest_key[gw] = best_key;
+    a.wbest_idx[gw] = best_idx;
+    a.wvalid[gw] = n_valid;
+  }
+}
+
+// ---- assignment oracle: thread per odometer index -------------------------
+struct OracleArgs {
+  int D, T, E;
+  const double* cost;
+  const double* w;
+  const int32_t* src;
+  const int32_t* dst;
+  const int32_t* eorder;
+  int64_t first, n;
+  uint64_t* bkey;
+  int64_t* bidx;
+};
+
+__global__ void oracle_kernel(const OracleArgs a) {
+  __shared__ uint64_t sk[256];
+  __shared__ int64_t si[256];
+  uint64_t bk = ~0ull;
+  int64_t bi = -1;
+  uint8_t dev[64];
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < a.n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t idx = a.first + k, r = idx;
+    for (int t = a.T - 1; t >= 0; --t) {
+      dev[t] = static_cast<uint8_t>(r % a.D);
+      r /= a.D;
+    }
+    double total = 0.0;  // objective_value order on the save-all cube
+    for (int d = 0; d < a.D; ++d)
+      for (int t = 0; t < a.T; ++t)
+        if (dev[t] == d) total = __dadd_rn(total, a.cost[d * a.T + t]);
+    for (int q = 0; q < a.E; ++q) {
+      const int e = a.eorder[q];
+      const int du = dev[a.src[e]], dv = dev[a.dst[e]];
+      if (du != dv) total = __dadd_rn(total, a.w[(e * a.D + du) * a.D + dv]);
+    }
+    const uint64_t key = __double_as_longlong(total);
+    if (key < bk || (key == bk && idx < bi)) {
+      bk = key;
+      bi = idx;
+    }
+  }
+  sk[threadIdx.x] = bk;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const uint64_t ok = sk[threadIdx.x + s];
+      const int64_t oi = si[threadIdx.x + s];
+      if (oi >= 0 && (ok < sk[threadIdx.x] || (ok == sk[threadIdx.x] && (si[threadIdx.x] < 0 || oi < si[threadIdx.x])))) {
+        sk[threadIdx.x] = ok;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.bkey[blockIdx.x] = sk[0];
+    a.bidx[blockIdx.x] = si[0];
+  }
+}
+
+}  // namespace place
+
+namespace {
+
+std::vector<int32_t> edges_by_dst(const HostProblem& h) {
+  std::vector<int32_t> o(static_cast<size_t>(h.E));
+  for (int e = 0; e < h.E; ++e) o[static_cast<size_t>(e)] = e;
+  std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return h.dst[static_cast<size_t>(a)] < h.dst[static_cast<size_t>(b)]; });
+  return o;
+}
+
+}  // namespace
+
+void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n, int policy, double* obj,
+                            int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3,
+                            unsigned char* scratch, cudaStream_t s) {
+  const HostProblem& h = pr->h;
+  if (!h.missing_link.empty() && h.D > 1) fail(XE_ERR_MISSING_LINK, h.missing_link);
+  if (h.D > 8) fail(XE_ERR_TOO_LARGE, "placement evaluation supports D <= 8");
+  if (policy != 0 && policy != 1) fail(XE_ERR_ARG, "policy must be 0 (save-all) or 1 (minimal-save)");
+  DevBuf<int32_t> eorder, last;
+  eorder.upload(h.E ? edges_by_dst(h) : std::vector<int32_t>(1, 0), s);
+  std::vector<int32_t> lst(static_cast<size_t>(h.T), -1);
+  for (int e = 0; e < h.E; ++e)
+    lst[static_cast<size_t>(h.src[static_cast<size_t>(e)])] =
+        std::max(lst[static_cast<size_t>(h.src[static_cast<size_t>(e)])], h.dst[static_cast<size_t>(e)]);
+  last.upload(lst, s);
+  std::vector<int32_t> lvp(static_cast<size_t>(h.T) + 1, 0), lvo;
+  for (int u = 0; u < h.T; ++u)
+    if (lst[static_cast<size_t>(u)] >= 0) lvp[static_cast<size_t>(lst[static_cast<size_t>(u)]) + 1]++;
+  for (int t = 0; t < h.T; ++t) lvp[static_cast<size_t>(t) + 1] += lvp[static_cast<size_t>(t)];
+  lvo.assign(static_cast<size_t>(std::max(1, lvp.back())), 0);
+  {
+    std::vector<int32_t> fill(lvp.begin(), lvp.end() - 1);
+    for (int u = 0; u < h.T; ++u)
+      if (lst[static_cast<size_t>(u)] >= 0) lvo[static_cast<size_t>(fill[static_cast<size_t>(lst[static_cast<size_t>(u)])]++)] = u;
+  }
+  DevBuf<int32_t> lv_ptr, lv_ops;
+  lv_ptr.upload(lvp, s);
+  lv_ops.upload(lvo, s);
+  place::Args a{};
+  a.D = h.D;
+  a.T = h.T;
+  a.E = h.E;
+  a.policy = policy;
+  a.fix_k = pr->fix_k_plain;
+  a.mass = pr->d_mass.p;
+  a.cost = pr->d_cost.p;
+  a.w = pr->d_w.p;
+  a.tfix = pr->d_tfix_noenergy.p;
+  a.src = pr->d_src.p;
+  a.dst = pr->d_dst.p;
+  a.eorder = eorder.p;
+  a.last = last.p;
+  a.lv_ptr = lv_ptr.p;
+  a.lv_ops = lv_ops.p;
+  a.budget = pr->d_budget.p;
+  a.ubound = pr->d_ubound.p;
+  a.dev = dev;
+  a.n = n;
+  a.obj = obj;
+  a.peak = peak;
+  a.flags = flags;
+  a.valid_mask = valid_mask;
+  int nsm = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+  const size_t nw_max = static_cast<size_t>(nsm) * 8 * 8;
+  a.wbest_key = reinterpret_cast<uint64_t*>(scratch);
+  a.wbest_idx = reinterpret_cast<int64_t*>(scratch + nw_max * 8);
+  a.wvalid = reinterpret_cast<int64_t*>(scratch + nw_max * 16);
+  const int tb = (h.T + 15) & ~15;
+  const int smem = place::kWarps * (tb + 128);
+  const bool exact = pr->fix_k_plain >= 0;
+  auto k = exact ? place::place_kernel<true> : place::place_kernel<false>;
+  XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, place::kWarps * 32, smem));
+  const int64_t want = (n + place::kWarps - 1) / place::kWarps;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(nsm) * std::max(1, std::min(per_sm, 8)))));
+  if (n > 0) {
+    k<<<grid, place::kWarps * 32, smem, s>>>(a);
+    XE_CUDA(cudaGetLastError());
+  }
+  if (best3) {
+    extern void reduce_best_launch(const uint64_t* key, const int64_t* idx, const int64_t* valid, int n,
+                                   uint64_t* out, cudaStream_t s);
+    if (n > 0) {
+      reduce_best_launch(a.wbest_key, a.wbest_idx, a.wvalid, grid * place::kWarps, best3, s);
+    } else {
+      const uint64_t none[3] = {~0ull, ~0ull, 0ull};
+      XE_CUDA(cudaMemcpyAsync(best3, none, sizeof none, cudaMemcpyHostToDevice, s));
+    }
+  }
+  XE_CUDA(cudaStreamSynchronize(s));  // the order/last tables are call-local
+}
+
+void assignment_oracle_device(const xe_problem* pr, double* best_obj, int32_t* best_dev, int64_t* n_eval,
+                              cudaStream_t s) {
+  const HostProblem& h = pr->h;
+  if (!h.missing_link.empty() && h.D > 1) fail(XE_ERR_MISSING_LINK, h.missing_link);
+  if (h.T > 64) fail(XE_ERR_TOO_LARGE, "placement family too large to enumerate");
+  double combos = 1.0;
+  for (int i = 0; i < h.T; ++i) combos *= h.D;
+  // the reference stops at 4e6 (solver.cpp:49); the sweep goes to 2^40
+  if (combos > 1099511627776.0) fail(XE_ERR_TOO_LARGE, "placement family too large to enumerate");
+  const int64_t n = static_cast<int64_t>(combos);
+  DevBuf<int32_t> eorder;
+  eorder.upload(h.E ? edges_by_dst(h) : std::vector<int32_t>(1, 0), s);
+  place::OracleArgs a{};
+  a.D = h.D;
+  a.T = h.T;
+  a.E = h.E;
+  a.cost = pr->d_cost.p;
+  a.w = pr->d_w.p;
+  a.src = pr->d_src.p;
+  a.dst = pr->d_dst.p;
+  a.eorder = eorder.p;
+  int nsm = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, nsm * 16)));
+  DevBuf<uint64_t> bk;
+  DevBuf<int64_t> bi;
+  bk.alloc(static_cast<size_t>(grid));
+  bi.alloc(static_cast<size_t>(grid));
+  a.first = 0;
+  a.n = n;
+  a.bkey = bk.p;
+  a.bidx = bi.p;
+  place::oracle_kernel<<<grid, 256, 0, s>>>(a);
+  XE_CUDA(cudaGetLastError());
+  std::vector<uint64_t> hk(static_cast<size_t>(grid));
+  std::vector<int64_t> hi(static_cast<size_t>(grid));
+  XE_CUDA(cudaMemcpyAsync(hk.data(), bk.p, grid * 8, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaMemcpyAsync(hi.data(), bi.p, grid * 8, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaStreamSynchronize(s));
+  uint64_t key = ~0ull;
+  int64_t idx = -1;
+  for (int g = 0; g < grid; ++g)
+    if (hi[static_cast<size_t>(g)] >= 0 &&
+        (hk[static_cast<size_t>(g)] < key || (hk[static_cast<size_t>(g)] == key && hi[static_cast<size_t>(g)] < idx))) {
+      key = hk[static_cast<size_t>(g)];
+      idx = hi[static_cast<size_t>(g)];
+    }
+  std::memcpy(best_obj, &key, 8);
+  int64_t r = idx;
+  for (int t = h.T - 1; t >= 0; --t) {
+    best_dev[t] = static_cast<int32_t>(r % h.D);
+    r /= h.D;
+  }
+  *n_eval = n;
+}
+
+}  // namespace xe
