@@ -4,7 +4,7 @@
 // reduction.  The kernel is in eval_cube_kernel.cuh.
 #include <cstring>
 
-#include "eval_cube_kernel.cuh"
+#include "eval_cube_v3.cuh"
 
 namespace xe {
 namespace cube {
@@ -129,7 +129,7 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
   auto warp_total = [&](int c, int c2) {
     int x = align16(a.off_w_terms + 2 * kSlots * c);
     x = align16(x + 2 * kSlots * c2);
-    x = align16(x + kSlots * (8 + 4 + 4 + 4) + 8 * kSlots * P.D);
+    x = align16(x + kSlots * (8 + 4 + 4 + 4) + 8 * kSlots * P.D + 2 * 32 * kCopyScratch);
     return x;
   };
   // prefer two resident CTAs per SM (occupancy), else the most warps that fit
