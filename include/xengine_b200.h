@@ -182,6 +182,25 @@ int xe_csr_get_csc(const xe_csr* m, const int64_t** col_ptr, const int32_t** row
 /* Bit-exact write_mps (mps_io.cpp:109-199) of the model.  Two-call: pass
  * buf = NULL to get the size in *len, then a buffer of *len bytes. */
 int xe_write_mps(xe_csr* m, char* buf, size_t* len);
+/* Host copy of the model; any NULL member is skipped.  Sizes from
+ * xe_csr_get_info (n_rows + 1 row offsets, nnz entries, n_cols columns). */
+typedef struct xe_csr_host {
+  int64_t* row_ptr; int32_t* col; double* val; double* rhs; int8_t* sense;
+  uint8_t* tag; int32_t* ordinal; double* obj; uint8_t* obj_present;
+  double* lb; double* ub; uint8_t* kind;
+} xe_csr_host;
+int xe_csr_download(const xe_csr* m, const xe_csr_host* out);
+/* A model handle from host arrays (a MilpModel the caller built or edited;
+ * columns in the closed-form VarRef space of p).  Every xe_csr_host member
+ * must be non-NULL; lb/ub/kind/obj/obj_present have n_cols entries. */
+int xe_csr_upload(const xe_problem* p, const xe_model_opts* opts, int64_t n_rows, int64_t n_cols,
+                  const xe_csr_host* in, xe_csr** out);
+/* Row part of check_assignment (model.cpp:449-467) for a dense column vector
+ * x (host [n_cols], VarRef order): per row the sequential lhs in term order,
+ * scale = max(1, |rhs|, max |term|), violated when the relation's excess
+ * exceeds tol*scale.  viol (host [n_rows] or NULL) receives the excess of
+ * violated rows and 0 elsewhere; *n_violated the count. */
+int xe_check_rows(xe_csr* m, const double* x, double tol, double* viol, int64_t* n_violated);
 /* Time of the last K1 assembly (device, CUDA events), milliseconds. */
 int xe_csr_last_build_ms(const xe_csr* m, float* ms);
 
@@ -211,9 +230,26 @@ typedef struct xe_best {
 int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                   int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best,
                   void* stream);
-/* Same, host buffers: copies in/out inside the call (the end-to-end path). */
+/* Same, host buffers: copies in/out inside the call (the end-to-end path).
+ * Host->device copies are pipelined in chunks over two streams; page-locked
+ * buffers (cudaHostAlloc / torch pin_memory) are DMA'd directly. */
 int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                        int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best);
+
+/* Candidate-interleaved layout ("xe_cube_il", T <= 64, D <= 8): the native
+ * layout of the lane-per-candidate evaluator.  u64 bit row (which, d, t) of
+ * candidate c (which 0 = R, 1 = S) is at
+ *     il[((c / 32) * K + (which * D + d) * T + t) * 32 + c % 32],  K = 2*D*T,
+ * so a warp reading one row of 32 candidates touches one 256-byte line.
+ * Buffers hold ceil(n/32)*32 candidates (padding lanes are ignored).
+ * xe_eval_cubes / xe_eval_cubes_host transpose canonical cubes into this
+ * layout internally when T <= 64. */
+size_t xe_cube_il_bytes(int32_t D, int32_t T, int64_t n);
+/* canonical device cubes [n] -> interleaved device buffer (xe_cube_il_bytes) */
+int xe_cubes_to_il(const xe_problem* p, const uint32_t* cubes, int64_t n, uint64_t* il, void* stream);
+/* Evaluates n interleaved device candidates; same outputs as xe_eval_cubes. */
+int xe_eval_cubes_il(const xe_problem* p, const xe_model_opts* opts, const uint64_t* il, int64_t n,
+                     xe_eval_out* out, uint32_t valid_mask, xe_best* best, void* stream);
 
 /* Placement candidates: dev[n][T] uint8 device per operator (save_all_assignment,
  * solver.cpp:30-42).  policy 0 = save-all (the reference's family),
@@ -224,6 +260,15 @@ int xe_eval_placements(const xe_problem* p, const uint8_t* dev, int64_t n, int32
  * placements in odometer order; writes the winning device vector. */
 int xe_assignment_oracle(const xe_problem* p, double* best_obj, int32_t* best_dev,
                          int64_t* n_evaluated);
+
+/* ---- single assignments (the map-based reference API) -------------------
+ * Dense column vectors x[n_cols] in VarRef order (model.hpp:18-24):
+ * R, S, Z [D][T][T]; F [D][T][E+T]; U [D][T][T]; P [T][E][D][D-1]. */
+int64_t xe_model_cols(int32_t D, int32_t T, int32_t E);
+/* complete_assignment (model.cpp:471-549) of one canonical host cube. */
+int xe_complete_cube(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cube, double* x);
+/* objective_value (model.cpp:369-428) of any x, same sequential fp64 order. */
+int xe_objective_dense(const xe_problem* p, const xe_model_opts* opts, const double* x, double* obj);
 
 /* ---- K3: PDHG LP relaxation -------------------------------------------- */
 typedef struct xe_pdhg_opts {

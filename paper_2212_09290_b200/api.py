@@ -180,6 +180,44 @@ def evaluate_cubes(problem: Problem, cubes, opts: Optional[ModelOptions] = None,
     return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
 
 
+def cubes_to_il(problem: Problem, cubes, out=None, stream=None):
+    """Canonical device cubes [n, cube_words] -> the interleaved layout
+    (xe_cube_il: 32-candidate groups, one u64 bit row per (R|S, d, t))."""
+    import torch
+    n = cubes.shape[0]
+    words = LIB.xe_cube_il_bytes(problem.D, problem.T, n) // 8
+    if out is None:
+        out = torch.empty(words, dtype=torch.int64, device=cubes.device)
+    s = stream if stream is not None else torch.cuda.current_stream(cubes.device).cuda_stream
+    check(LIB.xe_cubes_to_il(problem.handle, C.c_void_p(cubes.data_ptr()), n, C.c_void_p(out.data_ptr()),
+                             C.c_void_p(s)))
+    return out
+
+
+def evaluate_cubes_il(problem: Problem, il, n: int, opts: Optional[ModelOptions] = None,
+                      valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True, stream=None,
+                      out=None, best: bool = True):
+    """Evaluate n interleaved device candidates (cubes_to_il / round_cubes(layout="il"));
+    same results as evaluate_cubes on the canonical layout."""
+    import torch
+    opts = opts or ModelOptions()
+    dev = il.device
+    if out is not None:
+        obj, peak, flags = out
+    else:
+        obj = torch.empty(n, dtype=torch.float64, device=dev) if outputs else None
+        peak = torch.empty((n, problem.D), dtype=torch.int64, device=dev) if outputs else None
+        flags = torch.empty(n, dtype=torch.int32, device=dev) if outputs else None
+    eo = _lib.EvalOut(_ptr(obj), _ptr(peak), _ptr(flags))
+    b = _lib.Best()
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    check(LIB.xe_eval_cubes_il(problem.handle, C.byref(opts.c()), C.c_void_p(il.data_ptr()), n,
+                               C.byref(eo), valid_mask, C.byref(b) if best else None, C.c_void_p(s)))
+    if not best:
+        return EvalResult(obj, peak, flags, float("nan"), -1, -1)
+    return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
+
+
 class _DevArray:
     """__cuda_array_interface__ view of a device pointer owned by the library."""
 
@@ -320,6 +358,9 @@ def evaluate_cubes_host(problem: Problem, cubes: np.ndarray, opts: Optional[Mode
                         valid_mask: int = _lib.F_CHECK_MASK, outputs: bool = True):
     """End-to-end path: host cubes -> host results (copies inside the call)."""
     opts = opts or ModelOptions()
+    cubes = np.ascontiguousarray(cubes)
+    if cubes.dtype == np.int32:
+        cubes = cubes.view(np.uint32)  # same bits; keeps a pinned buffer pinned (no conversion copy)
     cubes = np.ascontiguousarray(cubes, np.uint32).reshape(-1, problem.cube_words)
     n = cubes.shape[0]
     obj = np.empty(n, np.float64) if outputs else None

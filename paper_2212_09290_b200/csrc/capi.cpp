@@ -31,6 +31,10 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
 void assignment_oracle_device(const xe_problem* pr, double* best_obj, int32_t* best_dev, int64_t* n_eval,
                               cudaStream_t s);
 
+int64_t model_cols(int D, int T, int E);  // complete.cu
+void complete_cube_host(const xe_problem* pr, const xe_model_opts& o, const uint32_t* cube_host, double* x_host);
+double objective_dense_host(const xe_problem* pr, const xe_model_opts& o, const double* x_host);
+
 namespace {
 
 void require_device(int device) {
@@ -108,6 +112,36 @@ void read_best(const uint64_t* dev3, cudaStream_t s, xe_best* best) {
   double o;
   std::memcpy(&o, &hb[0], 8);
   best->obj = best->index >= 0 ? o : INFINITY;
+}
+
+// Candidates per staging chunk of the canonical/host paths: ~64 MB of cubes.
+int64_t stage_chunk(const HostProblem& h) {
+  const size_t cb = xe_cube_bytes(h.D, h.T);
+  const int64_t c = static_cast<int64_t>((64ull << 20) / cb);
+  return std::max<int64_t>(32, c & ~int64_t{31});
+}
+
+// Best over per-chunk (objective bits, chunk-local index, valid count)
+// triples; chunks ascend in candidate index, so a strict < keeps the first.
+void combine_chunks(const uint64_t* dev, int64_t nchunks, int64_t chunk, cudaStream_t s, xe_best* best) {
+  std::vector<uint64_t> hb(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+  if (nchunks) {
+    XE_CUDA(cudaMemcpyAsync(hb.data(), dev, static_cast<size_t>(nchunks) * 24, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaStreamSynchronize(s));
+  }
+  best->index = -1;
+  best->n_valid = 0;
+  best->obj = INFINITY;
+  uint64_t bk = ~0ull;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t idx = static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 1)]);
+    best->n_valid += static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 2)]);
+    if (idx >= 0 && hb[static_cast<size_t>(3 * c)] < bk) {
+      bk = hb[static_cast<size_t>(3 * c)];
+      best->index = c * chunk + idx;
+      std::memcpy(&best->obj, &bk, 8);
+    }
+  }
 }
 
 }  // namespace
@@ -190,6 +224,8 @@ int xe_problem_destroy(xe_problem* p) {
     if (p->device >= 0) {
       cudaSetDevice(p->device);
       if (p->stream) cudaStreamDestroy(p->stream);
+      for (auto& st : p->stage)
+        if (st.stream) cudaStreamDestroy(st.stream);
     }
     delete p;
   });
@@ -242,89 +278,120 @@ int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t
     xe_model_opts o = opts_or_default(opts);
     auto* mp = const_cast<xe_problem*>(p);
     uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
-    eval_cubes_device(p, o, cubes, n, out ? out->obj : nullptr, out ? out->peak : nullptr,
-                      out ? out->flags : nullptr, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+    double* obj = out ? out->obj : nullptr;
+    int64_t* peak = out ? out->peak : nullptr;
+    uint32_t* flags = out ? out->flags : nullptr;
+    if (!il_supported(p)) {  // T > 64: the warp-per-candidate kernel on the canonical layout
+      eval_cubes_device(p, o, cubes, n, obj, peak, flags, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+      if (best) read_best(best3, s, best);
+      return;
+    }
+    // canonical -> interleaved in chunks of a stream-ordered staging buffer,
+    // then the lane-per-candidate evaluator
+    const HostProblem& h = p->h;
+    const size_t cw = xe_cube_bytes(h.D, h.T) / 4;
+    const int64_t chunk = stage_chunk(h);
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    auto& st = mp->stage[0];
+    st.il.reserve(il_bytes(h.D, h.T, std::min(chunk, std::max<int64_t>(n, 1))) / 8);
+    if (best) mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+      cubes_to_il_device(p, cubes + lo * cw, m, st.il.p, s);
+      eval_il_device(p, o, st.il.p, m, obj ? obj + lo : nullptr, peak ? peak + lo * h.D : nullptr,
+                     flags ? flags + lo : nullptr, valid_mask, best ? mp->chunk_best.p + 3 * c : nullptr,
+                     mp->scratch.p, s);
+    }
+    if (best) combine_chunks(mp->chunk_best.p, nchunks, chunk, s, best);
+  });
+}
+
+int xe_eval_cubes_il(const xe_problem* p, const xe_model_opts* opts, const uint64_t* il, int64_t n,
+                     xe_eval_out* out, uint32_t valid_mask, xe_best* best, void* stream) {
+  return guard([&] {
+    if (!p || (!il && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    xe_model_opts o = opts_or_default(opts);
+    auto* mp = const_cast<xe_problem*>(p);
+    uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
+    eval_il_device(p, o, il, n, out ? out->obj : nullptr, out ? out->peak : nullptr, out ? out->flags : nullptr,
+                   valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
     if (best) read_best(best3, s, best);
   });
 }
 
-// End-to-end path: host candidates in, host results out.  Chunks are
-// pipelined over two streams so the host->device copy of chunk k+1 overlaps
-// the evaluation of chunk k.
+size_t xe_cube_il_bytes(int32_t D, int32_t T, int64_t n) { return il_bytes(D, T, n); }
+
+int xe_cubes_to_il(const xe_problem* p, const uint32_t* cubes, int64_t n, uint64_t* il, void* stream) {
+  return guard([&] {
+    if (!p || ((!cubes || !il) && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    cubes_to_il_device(p, cubes, n, il, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// End-to-end path: host candidates in, host results out.  Chunks alternate
+// between two streams with their own staging buffers, so the host->device
+// copy of chunk k+1 overlaps the transpose + evaluation of chunk k.
 int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                        int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best) {
   return guard([&] {
     if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
     require_uploaded(p);
     xe_model_opts o = opts_or_default(opts);
+    auto* mp = const_cast<xe_problem*>(p);
     const HostProblem& h = p->h;
+    const bool il = il_supported(p);
     const size_t cb = xe_cube_bytes(h.D, h.T);
-    const int64_t chunk = std::max<int64_t>(1024, static_cast<int64_t>((256ull << 20) / cb));
+    const int64_t chunk = il ? stage_chunk(h) : std::max<int64_t>(1024, static_cast<int64_t>((256ull << 20) / cb));
     const int64_t nchunks = (n + chunk - 1) / chunk;
-    cudaStream_t st[2];
-    XE_CUDA(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
-    XE_CUDA(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
-    struct Bufs {
-      DevBuf<uint32_t> cubes;
-      DevBuf<double> obj;
-      DevBuf<int64_t> peak;
-      DevBuf<uint32_t> flags;
-      DevBuf<unsigned char> scratch;
-    } b[2];
+    const int64_t cap = std::min(chunk, std::max<int64_t>(n, 1));
     const size_t sb = eval_scratch_bytes(p->device);
-    for (int k = 0; k < 2; ++k) {
-      b[k].cubes.alloc(static_cast<size_t>(std::min(chunk, std::max<int64_t>(n, 1))) * cb / 4);
-      if (out && out->obj) b[k].obj.alloc(static_cast<size_t>(chunk));
-      if (out && out->peak) b[k].peak.alloc(static_cast<size_t>(chunk) * h.D);
-      if (out && out->flags) b[k].flags.alloc(static_cast<size_t>(chunk));
-      b[k].scratch.alloc(sb);
+    for (auto& st : mp->stage) {
+      if (!st.stream) XE_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+      st.canon.reserve(static_cast<size_t>(cap) * cb / 4);
+      if (il) st.il.reserve(il_bytes(h.D, h.T, cap) / 8);
+      if (out && out->obj) st.obj.reserve(static_cast<size_t>(cap));
+      if (out && out->peak) st.peak.reserve(static_cast<size_t>(cap) * h.D);
+      if (out && out->flags) st.flags.reserve(static_cast<size_t>(cap));
+      st.scratch.reserve(sb);
     }
-    DevBuf<uint64_t> best_all;
-    best_all.alloc(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+    mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+    // the two stages' streams must not start before work already queued on
+    // the handle's stream (previous calls) has finished with the buffers
+    XE_CUDA(cudaStreamSynchronize(p->stream));
     try {
       for (int64_t c = 0; c < nchunks; ++c) {
-        const int k = static_cast<int>(c & 1);
+        auto& st = mp->stage[c & 1];
         const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
-        h2d(b[k].cubes.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
-            st[k]);
-        eval_cubes_device(p, o, b[k].cubes.p, m, b[k].obj.p, b[k].peak.p, b[k].flags.p, valid_mask,
-                          best_all.p + 3 * c, b[k].scratch.p, st[k]);
-        if (out && out->obj)
-          XE_CUDA(cudaMemcpyAsync(out->obj + lo, b[k].obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st[k]));
-        if (out && out->peak)
-          XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, b[k].peak.p, m * h.D * sizeof(int64_t),
-                                  cudaMemcpyDeviceToHost, st[k]));
-        if (out && out->flags)
-          XE_CUDA(cudaMemcpyAsync(out->flags + lo, b[k].flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, st[k]));
-      }
-      XE_CUDA(cudaStreamSynchronize(st[0]));
-      XE_CUDA(cudaStreamSynchronize(st[1]));
-      if (best) {
-        std::vector<uint64_t> hb(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
-        if (nchunks) XE_CUDA(cudaMemcpy(hb.data(), best_all.p, hb.size() * 8, cudaMemcpyDeviceToHost));
-        best->index = -1;
-        best->n_valid = 0;
-        best->obj = INFINITY;
-        uint64_t bk = ~0ull;
-        for (int64_t c = 0; c < nchunks; ++c) {
-          const int64_t idx = static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 1)]);
-          best->n_valid += static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 2)]);
-          if (idx >= 0 && hb[static_cast<size_t>(3 * c)] < bk) {  // chunks ascend in index: strict <
-            bk = hb[static_cast<size_t>(3 * c)];
-            best->index = c * chunk + idx;
-            std::memcpy(&best->obj, &bk, 8);
-          }
+        h2d(st.canon.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
+            st.stream);
+        if (il) {
+          cubes_to_il_device(p, st.canon.p, m, st.il.p, st.stream);
+          eval_il_device(p, o, st.il.p, m, st.obj.p, st.peak.p, st.flags.p, valid_mask, mp->chunk_best.p + 3 * c,
+                         st.scratch.p, st.stream);
+        } else {
+          eval_cubes_device(p, o, st.canon.p, m, st.obj.p, st.peak.p, st.flags.p, valid_mask,
+                            mp->chunk_best.p + 3 * c, st.scratch.p, st.stream);
         }
+        if (out && out->obj)
+          XE_CUDA(cudaMemcpyAsync(out->obj + lo, st.obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st.stream));
+        if (out && out->peak)
+          XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, st.peak.p, m * h.D * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, st.stream));
+        if (out && out->flags)
+          XE_CUDA(cudaMemcpyAsync(out->flags + lo, st.flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                  st.stream));
       }
+      XE_CUDA(cudaStreamSynchronize(mp->stage[0].stream));
+      XE_CUDA(cudaStreamSynchronize(mp->stage[1].stream));
     } catch (...) {
-      cudaStreamSynchronize(st[0]);
-      cudaStreamSynchronize(st[1]);
-      cudaStreamDestroy(st[0]);
-      cudaStreamDestroy(st[1]);
+      cudaStreamSynchronize(mp->stage[0].stream);
+      cudaStreamSynchronize(mp->stage[1].stream);
       throw;
     }
-    cudaStreamDestroy(st[0]);
-    cudaStreamDestroy(st[1]);
+    if (best) combine_chunks(mp->chunk_best.p, nchunks, chunk, p->stream, best);
   });
 }
 
@@ -349,6 +416,24 @@ int xe_eval_placements(const xe_problem* p, const uint8_t* dev, int64_t n, int32
     eval_placements_device(p, dev, n, policy, out ? out->obj : nullptr, out ? out->peak : nullptr,
                            out ? out->flags : nullptr, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
     if (best) read_best(best3, s, best);
+  });
+}
+
+int64_t xe_model_cols(int32_t D, int32_t T, int32_t E) { return model_cols(D, T, E); }
+
+int xe_complete_cube(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cube, double* x) {
+  return guard([&] {
+    if (!p || !cube || !x) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    complete_cube_host(p, opts_or_default(opts), cube, x);
+  });
+}
+
+int xe_objective_dense(const xe_problem* p, const xe_model_opts* opts, const double* x, double* obj) {
+  return guard([&] {
+    if (!p || !x || !obj) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(p);
+    *obj = objective_dense_host(p, opts_or_default(opts), x);
   });
 }
 

@@ -14,6 +14,7 @@ std::vector<T> down(const T* p, size_t n, cudaStream_t s) {
   return v;
 }
 }  // namespace
+int64_t check_rows_host(xe_csr* m, const double* x_host, double tol, double* viol_host);  // complete.cu
 }  // namespace xe
 
 using namespace xe;
@@ -86,6 +87,92 @@ int xe_csr_last_build_ms(const xe_csr* m, float* ms) {
   return guard([&] {
     if (!m || !ms) fail(XE_ERR_ARG, "null argument");
     *ms = m->build_ms;
+  });
+}
+
+int xe_csr_download(const xe_csr* m, const xe_csr_host* o) {
+  return guard([&] {
+    if (!m || !o) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(m->prob);
+    const xe_csr_info& in = m->info;
+    cudaStream_t s = m->stream;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) XE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    const size_t R = static_cast<size_t>(in.n_rows), Z = static_cast<size_t>(in.nnz), N = static_cast<size_t>(in.n_cols);
+    cp(o->row_ptr, m->row_ptr.p, (R + 1) * 8);
+    cp(o->col, m->col.p, Z * 4);
+    cp(o->val, m->val.p, Z * 8);
+    cp(o->rhs, m->rhs.p, R * 8);
+    cp(o->sense, m->sense.p, R);
+    cp(o->tag, m->tag.p, R);
+    cp(o->ordinal, m->ordinal.p, R * 4);
+    cp(o->obj, m->obj.p, N * 8);
+    cp(o->obj_present, m->present.p, N);
+    cp(o->lb, m->lb.p, N * 8);
+    cp(o->ub, m->ub.p, N * 8);
+    cp(o->kind, m->kind.p, N);
+    XE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int xe_csr_upload(const xe_problem* p, const xe_model_opts* opts, int64_t n_rows, int64_t n_cols,
+                  const xe_csr_host* in, xe_csr** out) {
+  return guard([&] {
+    if (!p || !in || !out || n_rows < 0) fail(XE_ERR_ARG, "null argument");
+    if (!in->row_ptr || !in->col || !in->val || !in->rhs || !in->sense || !in->tag || !in->ordinal || !in->obj ||
+        !in->obj_present || !in->lb || !in->ub || !in->kind)
+      fail(XE_ERR_ARG, "xe_csr_upload needs every xe_csr_host array");
+    require_uploaded(p);
+    const HostProblem& h = p->h;
+    if (n_cols != xe_model_cols(h.D, h.T, h.E)) fail(XE_ERR_DIMENSION_MISMATCH, "column count of the model space");
+    const int64_t nnz = in->row_ptr[n_rows];
+    for (int64_t k = 0; k < nnz; ++k)
+      if (in->col[k] < 0 || in->col[k] >= n_cols) fail(XE_ERR_UNKNOWN_VARIABLE, "column index outside the model");
+    auto m = std::make_unique<xe_csr>();
+    m->prob = p;
+    m->opts = opts ? *opts : xe_model_opts{};
+    m->stream = p->stream;
+    cudaStream_t s = m->stream;
+    auto up = [&](auto& buf, const auto* src, size_t count) {
+      buf.alloc(std::max<size_t>(1, count));
+      if (count) XE_CUDA(cudaMemcpyAsync(buf.p, src, count * sizeof(*src), cudaMemcpyHostToDevice, s));
+    };
+    const size_t R = static_cast<size_t>(n_rows), Z = static_cast<size_t>(nnz), N = static_cast<size_t>(n_cols);
+    up(m->row_ptr, in->row_ptr, R + 1);
+    up(m->col, in->col, Z);
+    up(m->val, in->val, Z);
+    up(m->rhs, in->rhs, R);
+    up(m->sense, in->sense, R);
+    up(m->tag, in->tag, R);
+    up(m->ordinal, in->ordinal, R);
+    up(m->obj, in->obj, N);
+    up(m->present, in->obj_present, N);
+    up(m->lb, in->lb, N);
+    up(m->ub, in->ub, N);
+    up(m->kind, in->kind, N);
+    xe_csr_info& info = m->info;
+    info.n_cols = n_cols;
+    info.n_rows = n_rows;
+    info.nnz = nnz;
+    info.D = h.D;
+    info.T = h.T;
+    info.E = h.E;
+    info.n_tags = 14;
+    std::memset(info.tag_rows, 0, sizeof info.tag_rows);
+    for (int64_t r = 0; r < n_rows; ++r)
+      if (in->tag[r] < 16) info.tag_rows[in->tag[r]]++;
+    info.n_rows_mps = n_rows - (m->opts.quadratic_objective ? info.tag_rows[11] : 0);
+    XE_CUDA(cudaStreamSynchronize(s));
+    *out = m.release();
+  });
+}
+
+int xe_check_rows(xe_csr* m, const double* x, double tol, double* viol, int64_t* n_violated) {
+  return guard([&] {
+    if (!m || !x || !n_violated) fail(XE_ERR_ARG, "null argument");
+    require_uploaded(m->prob);
+    *n_violated = check_rows_host(m, x, tol, viol);
   });
 }
 

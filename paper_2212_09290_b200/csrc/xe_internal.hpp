@@ -75,6 +75,11 @@ struct DevBuf {
     if (count) XE_CUDA(cudaMalloc(&p, count * sizeof(T)));
     n = count;
   }
+  // grow-only: keeps the buffer when it already holds count elements
+  void reserve(size_t count) {
+    if (p && count <= n) return;
+    alloc(count);
+  }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     alloc(v.size());
     if (!v.empty()) XE_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -158,10 +163,30 @@ struct xe_problem {
   xe::DevProblem view(bool energy) const;
   // scratch for batched evaluation
   xe::DevBuf<uint8_t> scratch;
+  // persistent staging of the canonical-layout and host entry points
+  // (xe_eval_cubes, xe_eval_cubes_host): grown on demand, reused across calls
+  struct Stage {
+    xe::DevBuf<uint32_t> canon;
+    xe::DevBuf<uint64_t> il;
+    xe::DevBuf<double> obj;
+    xe::DevBuf<int64_t> peak;
+    xe::DevBuf<uint32_t> flags;
+    xe::DevBuf<uint8_t> scratch;
+    cudaStream_t stream = nullptr;
+  };
+  Stage stage[2];
+  xe::DevBuf<uint64_t> chunk_best;  // [chunks][3] best-of-chunk triples
 };
 
 namespace xe {
 void upload_problem(xe_problem* p);   // problem.cu
+// eval_il.cu: lane-per-candidate evaluator over the interleaved layout
+bool il_supported(const xe_problem* pr);
+size_t il_bytes(int D, int T, int64_t n);
+void cubes_to_il_device(const xe_problem* pr, const uint32_t* cubes, int64_t n, uint64_t* il, cudaStream_t s);
+void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint64_t* il, int64_t n, double* obj,
+                    int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3, unsigned char* scratch,
+                    cudaStream_t stream);
 void require_uploaded(const xe_problem* p);  // capi.cpp: device handle + cudaSetDevice
 int exact_fix_k(const std::vector<double>& table, int T);
 }  // namespace xe

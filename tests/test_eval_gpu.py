@@ -101,3 +101,28 @@ def test_unaligned_and_odd_sizes(oracle):
     t = torch.zeros((0, prob.cube_words), dtype=torch.int32, device="cuda")
     r = xe.evaluate_cubes(prob, t)
     assert r.best_index == -1 and r.n_valid == 0
+
+
+@pytest.mark.parametrize("name", ["fig2", "vgg16", "rand3", "chain3"])
+def test_interleaved_layout_matches_canonical(oracle, name):
+    """xe_cube_il (lane-per-candidate kernel fed directly) == the canonical
+    entry point == the CPU oracle, including a ragged last group."""
+    text = doc(name)
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    n = 1000 + 13
+    cubes = cubegen.mixed_cubes(a, n, seed=7, random_frac=0.05)
+    t = torch.from_numpy(cubes.view(np.int32)).cuda()
+    il = xe.cubes_to_il(prob, t)
+    assert il.numel() * 8 == ((n + 31) // 32) * 32 * 2 * prob.D * prob.T * 8
+    for strict in (0, 1):
+        opts = xe.ModelOptions(strict_free=bool(strict))
+        r = xe.evaluate_cubes_il(prob, il, n, opts)
+        o, p, f, rc = run_gpu(prob, cubes, strict)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
+        assert np.array_equal(r.peak.cpu().numpy(), p)
+        assert np.array_equal(r.flags.cpu().numpy().view(np.uint32), f)
+        assert (r.best_index, r.n_valid) == (rc.best_index, rc.n_valid)
+        ro, rp, rf = oracle.eval_cubes(a, cubes, strict)
+        compare(o, p, f, ro, rp, rf)
