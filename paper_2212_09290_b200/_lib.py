@@ -92,6 +92,10 @@ class CsrView(C.Structure):
         "lb", "ub", "kind")]
 
 
+class CsrHost(CsrView):
+    """xe_csr_host: the same twelve arrays, host pointers."""
+
+
 class PdhgOpts(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("tol_rel", C.c_double),
                 ("check_every", C.c_int32), ("verbose", C.c_int32),
@@ -134,6 +138,12 @@ SIGNATURES = {
     "xe_cubes_to_il": (C.c_int, [P, P, C.c_int64, P, P]),
     "xe_eval_cubes_il": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, C.POINTER(EvalOut),
                                    C.c_uint32, C.POINTER(Best), P]),
+    "xe_csr_download": (C.c_int, [P, C.POINTER(CsrHost)]),
+    "xe_csr_upload": (C.c_int, [P, C.POINTER(ModelOpts), C.c_int64, C.c_int64, C.POINTER(CsrHost), C.POINTER(P)]),
+    "xe_check_rows": (C.c_int, [P, P, C.c_double, P, C.POINTER(C.c_int64)]),
+    "xe_model_cols": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "xe_complete_cube": (C.c_int, [P, C.POINTER(ModelOpts), P, P]),
+    "xe_objective_dense": (C.c_int, [P, C.POINTER(ModelOpts), P, C.POINTER(C.c_double)]),
     "xe_eval_placements": (C.c_int, [P, P, C.c_int64, C.c_int32, C.POINTER(EvalOut), C.c_uint32,
                                      C.POINTER(Best), P]),
     "xe_assignment_oracle": (C.c_int, [P, C.POINTER(C.c_double), P, C.POINTER(C.c_int64)]),
