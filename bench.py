@@ -137,6 +137,7 @@ def main():
     from paper_2212_09290_b200 import _lib
     from bench import configs
     from bench.clocks import ClockSampler
+    from paper_2212_09290_b200.shard import exchange_best
 
     doc = configs.vgg16_doc()
     prob = xe.Problem.from_json(doc, device=local)
@@ -200,16 +201,10 @@ def main():
     best_obj, best_idx = r.best_obj, r.best_index
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        # incumbent exchange: min objective bits, then min global index among equals
-        key = torch.tensor([np.float64(best_obj).view(np.int64) if best_idx >= 0 else np.iinfo(np.int64).max],
-                           dtype=torch.int64, device="cuda")
-        mine = key.clone()
-        dist.all_reduce(key, op=dist.ReduceOp.MIN)
-        gidx = torch.tensor([rank * n + best_idx if (best_idx >= 0 and int(mine) == int(key)) else np.iinfo(np.int64).max],
-                            dtype=torch.int64, device="cuda")
-        dist.all_reduce(gidx, op=dist.ReduceOp.MIN)
-        best_idx = int(gidx)
-        best_obj = float(np.int64(int(key)).view(np.float64)) if best_idx < np.iinfo(np.int64).max else float("inf")
+        # incumbent exchange: MIN of objective bits, then MIN global index
+        # among ranks holding it, SUM of valid counts (shard.py)
+        inc = exchange_best(best_obj, best_idx, r.n_valid, offset=rank * n, device="cuda")
+        best_obj, best_idx = inc.obj, inc.index
     step_ms, kern_ms = float(t[0]), float(t[1])
     value = world * n / (step_ms / 1e3)
 

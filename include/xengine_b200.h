@@ -286,6 +286,11 @@ typedef struct xe_pdhg_result {
   int32_t iters, restarts, status; /* 0 converged, 1 iteration limit */
   double solve_ms;           /* device time, CUDA events */
   double spmv_ms_per_iter;
+  /* presolve: columns with the prohibitive cost (>= 1e9, problem.hpp:16) and
+   * lower bound 0 are fixed at 0 during the solve; `certified` = 1 when the
+   * final duals price every fixed column non-negatively (reduced cost
+   * 1e9 - K'y >= 0), i.e. the fixing provably left the LP optimum unchanged */
+  int32_t presolve_fixed, certified;
 } xe_pdhg_result;
 
 int xe_pdhg_solve(xe_csr* m, const xe_pdhg_opts* opts, xe_pdhg_result* res,

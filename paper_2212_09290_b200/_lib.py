@@ -107,7 +107,8 @@ class PdhgResult(C.Structure):
                 ("rel_gap", C.c_double), ("rel_primal_res", C.c_double),
                 ("rel_dual_res", C.c_double), ("iters", C.c_int32),
                 ("restarts", C.c_int32), ("status", C.c_int32),
-                ("solve_ms", C.c_double), ("spmv_ms_per_iter", C.c_double)]
+                ("solve_ms", C.c_double), ("spmv_ms_per_iter", C.c_double),
+                ("presolve_fixed", C.c_int32), ("certified", C.c_int32)]
 
 
 # symbol -> (restype, argtypes); the set of exports include/xengine_b200.h declares

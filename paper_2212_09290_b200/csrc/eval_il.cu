@@ -58,8 +58,21 @@ struct IlArgs {
   int64_t* wvalid;
   int copy_in_smem;  // 1: the copy-term table fits in shared memory
   int off_mass, off_pmask, off_cons, off_mtab, off_tab, off_inptr, off_inedge, off_src, off_dst,
-      off_ebad, off_q, smem_bytes;
+      off_ebad, off_q, off_warp, warp_bytes, smem_bytes, q_cap;
 };
+
+// Rows holding >= 2 computations (recompute edits) need the free walk of
+// row_peak_nw1; a lane meeting one defers it to a per-warp queue, and the
+// warp drains the queue one row per lane, so the walk runs at full width
+// instead of at the pace of the slowest lane every timestep.
+struct PeakRow {
+  uint64_t r, z, sn, scan;
+  int64_t base;
+  int32_t owner;  // lane * MAXD + d
+  int32_t pad;
+};
+// queue capacity: one timestep can add up to 32 * D rows
+inline int queue_cap(int D) { return 32 * (D <= 4 ? D : 8) + 32; }
 
 __device__ __forceinline__ int64_t mass_of_bits(uint64_t w, const int64_t* mass) {
   int64_t s = 0;
@@ -76,10 +89,10 @@ __device__ __forceinline__ int64_t mass_of_bits(uint64_t w, const int64_t* mass)
 // the allocation; F(u->b) fires for u in parents(b) + {b} that is resident,
 // not kept (S(d,t+1,u) = 0) and has no consumer after b computed on d
 // (strict_free: on any device) — model.cpp:492-505, 521-537.
-__device__ __noinline__ int64_t row_peak_nw1(uint64_t r, uint64_t z, uint64_t sn, uint64_t scan, int64_t base,
-                                             int T, const uint64_t* s_pmask, const uint64_t* s_cons,
-                                             const int64_t* s_mass) {
-  int64_t cur = base, peak = base;
+template <class M>
+__device__ __noinline__ M row_peak_nw1(uint64_t r, uint64_t z, uint64_t sn, uint64_t scan, M base, int T,
+                                       const uint64_t* s_pmask, const uint64_t* s_cons, const M* s_mass) {
+  M cur = base, peak = base;
   for (uint64_t rem = r; rem; rem &= rem - 1) {
     const int b = __ffsll(rem) - 1;
     cur += s_mass[b];
@@ -92,6 +105,11 @@ __device__ __noinline__ int64_t row_peak_nw1(uint64_t r, uint64_t z, uint64_t sn
     }
   }
   return peak;
+}
+
+__device__ __forceinline__ void smem_max(int32_t* p, int32_t v) { atomicMax(p, v); }
+__device__ __forceinline__ void smem_max(int64_t* p, int64_t v) {
+  atomicMax(reinterpret_cast<long long*>(p), static_cast<long long>(v));
 }
 
 // EQ11 rows of timestep t (S(d,t+1,i) > S(d,t,i) + R(d,t,i)) and the EQ16_HI
@@ -148,18 +166,20 @@ __device__ __noinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t*
   return 0;
 }
 
-template <int MAXD>
-__global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
+// M: integer type of tensor masses and memory sums (int32 when twice the
+// save-all total fits, halving the table traffic; int64 otherwise).
+template <int MAXD, class M>
+__global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 4 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NW = 1;
   const DevProblem& P = a.P;
   const int D = cube::ndev<MAXD>(P), T = P.T, E = P.E;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
-  int64_t* s_mass = reinterpret_cast<int64_t*>(smem + a.off_mass);
+  M* s_mass = reinterpret_cast<M*>(smem + a.off_mass);
   uint64_t* s_pmask = reinterpret_cast<uint64_t*>(smem + a.off_pmask);
   uint64_t* s_cons = reinterpret_cast<uint64_t*>(smem + a.off_cons);
-  int64_t* s_mtab = reinterpret_cast<int64_t*>(smem + a.off_mtab);
+  M* s_mtab = reinterpret_cast<M*>(smem + a.off_mtab);
   double* s_tab = reinterpret_cast<double*>(smem + a.off_tab);
   int32_t* s_inptr = reinterpret_cast<int32_t*>(smem + a.off_inptr);
   int32_t* s_inedge = reinterpret_cast<int32_t*>(smem + a.off_inedge);
@@ -172,11 +192,11 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
   // memory; the copy terms [E*D*D] too when they fit, else read through L1
   const int n_dt = D * T, n_copy = E * D * D;
   for (int i = threadIdx.x; i < T; i += blockDim.x) {
-    s_mass[i] = P.mass[i];
+    s_mass[i] = static_cast<M>(P.mass[i]);
     s_pmask[i] = P.pmask[i];
     s_cons[i] = P.cons[i];
   }
-  for (int i = threadIdx.x; i < P.NB * 256; i += blockDim.x) s_mtab[i] = P.mtab[i];
+  for (int i = threadIdx.x; i < P.NB * 256; i += blockDim.x) s_mtab[i] = static_cast<M>(P.mtab[i]);
   for (int i = threadIdx.x; i < n_dt; i += blockDim.x) {
     s_tab[i] = P.table[i];
     if (a.energy) s_tab[n_dt + i] = P.table[n_dt + n_copy + i];
@@ -195,8 +215,22 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
     if (P.has_total)
       for (int i = threadIdx.x; i < n_dt; i += blockDim.x) s_q[i] = P.q[i];
   }
+  PeakRow* queue = reinterpret_cast<PeakRow*>(smem + a.off_warp + wid * a.warp_bytes);
+  M* s_pk = reinterpret_cast<M*>(queue + a.q_cap);  // [32][MAXD] deferred row peaks
+  for (int i = lane; i < 32 * MAXD; i += 32) s_pk[i] = 0;
   __syncthreads();
   const double* copy_tab = a.copy_in_smem ? s_copy : P.table + n_dt;
+  int q_cnt = 0;  // warp-uniform
+  auto drain = [&]() {
+    __syncwarp();
+    for (int k = lane; k < q_cnt; k += 32) {
+      const PeakRow q = queue[k];
+      const M rp = row_peak_nw1<M>(q.r, q.z, q.sn, q.scan, static_cast<M>(q.base), T, s_pmask, s_cons, s_mass);
+      smem_max(&s_pk[q.owner], rp);
+    }
+    __syncwarp();
+    q_cnt = 0;
+  };
 
   const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -216,11 +250,11 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
 
     uint32_t fl = 0;
     double total = 0.0;
-    int64_t pk[MAXD];
+    M pk[MAXD];
 #pragma unroll
     for (int d = 0; d < MAXD; ++d) pk[d] = 0;
 
-    if (live) {
+    {  // padding lanes of the last group evaluate their zero rows; results are dropped
       // ================= pass B: compute terms, d-major =================
       uint64_t diag = 0, multi = 0;
       int eq9 = 0;
@@ -301,20 +335,27 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
 #pragma unroll
         for (int d = 0; d < MAXD; ++d) {
           if (d >= D) continue;
-          int64_t base = 0;
+          M base = 0;
           const uint32_t lo = static_cast<uint32_t>(S[d]), hi = static_cast<uint32_t>(S[d] >> 32);
 #pragma unroll
           for (int b = 0; b < 8; ++b)
             if (b < P.NB) base += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
           const uint64_t r = R[d];
-          int64_t rp = base;
-          if (r & (r - 1)) {
-            rp = row_peak_nw1(r, R[d] | S[d], Sn[d], a.strict ? rany : r, base, T, s_pmask, s_cons, s_mass);
-          } else if (r) {
-            rp = base + s_mass[__ffsll(r) - 1];
+          const bool multi = (r & (r - 1)) != 0;
+          const unsigned ballot = __ballot_sync(0xffffffffu, multi);
+          if (multi) {
+            PeakRow& q = queue[q_cnt + __popc(ballot & ((1u << lane) - 1u))];
+            q.r = r;
+            q.z = R[d] | S[d];
+            q.sn = Sn[d];
+            q.scan = a.strict ? rany : r;
+            q.base = base;
+            q.owner = lane * MAXD + d;
           }
-          pk[d] = max(pk[d], rp);
+          q_cnt += __popc(ballot);
+          pk[d] = max(pk[d], r ? base + s_mass[__ffsll(r) - 1] : base);  // <= the deferred peak when multi
         }
+        if (q_cnt > a.q_cap - 32 * D) drain();
 
         // ---- the computations of timestep t: dependencies (EQ12), decode's
         // copy sources, and (edges sorted by dst) the copy charges in
@@ -331,8 +372,10 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
             if (x < D && x != d) elsewhere[d] |= R[x] | S[x];
         }
         bool copies_left = false;
-        for (uint64_t rem = rany; rem; rem &= rem - 1) {
-          const int v = __ffsll(rem) - 1;
+        // computations of t in ascending op order (the copy-charge order):
+        // recomputes below t, the diagonal op t (the same v for every lane),
+        // then any (fixed-zero violating) ops above t
+        auto visit = [&](int v) {
           const uint64_t pm = s_pmask[v];
           need_all |= pm;
           const bool le = v <= t;
@@ -344,10 +387,10 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
             if (le) needD[dc] |= pm;
             if (pm & elsewhere[dc]) cp = true;
           }
-          if (!cp) continue;
+          if (!cp) return;
           if (!by_dst) {
             copies_left = true;
-            continue;
+            return;
           }
           for (int k = s_inptr[v]; k < s_inptr[v + 1]; ++k) {
             const int e = s_inedge[k], u = s_src[e];
@@ -360,7 +403,11 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
                   total = __dadd_rn(total, copy_tab[(e * D + ds) * D + dc]);
             }
           }
-        }
+        };
+        const uint64_t below_t = (1ull << t) - 1ull;
+        for (uint64_t rem = rany & below_t; rem; rem &= rem - 1) visit(__ffsll(rem) - 1);
+        if ((rany >> t) & 1ull) visit(t);
+        for (uint64_t rem = rany & ~below_t & ~(1ull << t); rem; rem &= rem - 1) visit(__ffsll(rem) - 1);
         if (need_all & ~zany) fl |= XE_F_EQ12;
         if (need_le & ~zany) fl |= XE_F_DECODE;
         // a copy source can free its tensor within timestep t only if it
@@ -404,6 +451,13 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
         }
       }
 
+      if (q_cnt) drain();
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) {
+        pk[d] = max(pk[d], s_pk[lane * MAXD + d]);
+        s_pk[lane * MAXD + d] = 0;
+      }
+
       // ================= pass E: energy terms, d-major =================
       if (a.energy) {
         for (int d = 0; d < D; ++d) {
@@ -416,16 +470,16 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
 #pragma unroll
       for (int d = 0; d < MAXD; ++d) {
         if (d >= D) continue;
-        if (pk[d] > P.budget[d]) fl |= XE_F_BUDGET;
+        if (static_cast<int64_t>(pk[d]) > P.budget[d]) fl |= XE_F_BUDGET;
         if (static_cast<double>(pk[d]) > P.ubound[d]) fl |= XE_F_U_BOUND;
       }
-      if (a.obj) a.obj[c] = total;
-      if (a.flags) a.flags[c] = fl;
-      if (a.peak)
+      if (live && a.obj) a.obj[c] = total;
+      if (live && a.flags) a.flags[c] = fl;
+      if (live && a.peak)
 #pragma unroll
         for (int d = 0; d < MAXD; ++d)
-          if (d < D) a.peak[c * D + d] = pk[d];
-      if ((fl & a.valid_mask) == 0) {
+          if (d < D) a.peak[c * D + d] = static_cast<int64_t>(pk[d]);
+      if (live && (fl & a.valid_mask) == 0) {
         ++n_valid;
         const uint64_t key = __double_as_longlong(total);
         if (key < best_key) {  // candidates of a lane ascend: strict < keeps the first
@@ -484,9 +538,9 @@ __global__ void __launch_bounds__(256) to_il_kernel(const uint32_t* __restrict__
 
 int align16(int x) { return (x + 15) & ~15; }
 
-template <int MAXD>
-int launch(const IlArgs& a, cudaStream_t s, int nsm) {
-  auto k = eval_il_kernel<MAXD>;
+template <int MAXD, class M>
+int launch_m(const IlArgs& a, cudaStream_t s, int nsm) {
+  auto k = eval_il_kernel<MAXD, M>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes));
   int per_sm = 0;
   XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarps * 32, a.smem_bytes));
@@ -497,6 +551,11 @@ int launch(const IlArgs& a, cudaStream_t s, int nsm) {
   k<<<grid, kWarps * 32, a.smem_bytes, s>>>(a);
   XE_CUDA(cudaGetLastError());
   return grid;
+}
+
+template <int MAXD>
+int launch(const IlArgs& a, cudaStream_t s, int nsm, bool m32) {
+  return m32 ? launch_m<MAXD, int32_t>(a, s, nsm) : launch_m<MAXD, int64_t>(a, s, nsm);
 }
 
 }  // namespace il
@@ -544,11 +603,17 @@ void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint6
     off = align16(off + bytes);
     return o;
   };
+  // every U value is at most twice the save-all total (a tensor both saved
+  // and recomputed in one row is counted twice, model.cpp:517-537)
+  int64_t total_mass = 0;
+  for (int64_t m : h.mass) total_mass += m;
+  const bool m32 = total_mass < (int64_t{1} << 30);
+  const int msz = m32 ? 4 : 8;
   const int n_dt = P.D * P.T, n_copy = P.E * P.D * P.D;
-  a.off_mass = take(8 * P.T);
+  a.off_mass = take(msz * P.T);
   a.off_pmask = take(8 * P.T);
   a.off_cons = take(8 * P.T);
-  a.off_mtab = take(8 * 256 * P.NB);
+  a.off_mtab = take(msz * 256 * P.NB);
   a.off_inptr = take(4 * (P.T + 1));
   a.off_inedge = take(4 * std::max(1, P.E));
   a.off_src = take(4 * std::max(1, P.E));
@@ -557,7 +622,11 @@ void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint6
   a.off_q = take(a.energy && P.has_total ? 8 * n_dt : 8);
   a.copy_in_smem = (off + 8 * (2 * n_dt + n_copy) <= 64 * 1024) ? 1 : 0;
   a.off_tab = take(8 * (2 * n_dt + (a.copy_in_smem ? n_copy : 0)));
-  a.smem_bytes = off;
+  a.off_warp = off;
+  a.q_cap = queue_cap(P.D);
+  const int maxd = P.D <= 4 ? P.D : 8;
+  a.warp_bytes = align16(static_cast<int>(sizeof(PeakRow)) * a.q_cap + msz * 32 * maxd);
+  a.smem_bytes = off + kWarps * a.warp_bytes;
 
   int nsm = 0;
   XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
@@ -568,11 +637,11 @@ void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint6
   int grid = 0;
   if (n > 0) {
     switch (P.D) {
-      case 1: grid = launch<1>(a, stream, nsm); break;
-      case 2: grid = launch<2>(a, stream, nsm); break;
-      case 3: grid = launch<3>(a, stream, nsm); break;
-      case 4: grid = launch<4>(a, stream, nsm); break;
-      default: grid = launch<8>(a, stream, nsm); break;
+      case 1: grid = launch<1>(a, stream, nsm, m32); break;
+      case 2: grid = launch<2>(a, stream, nsm, m32); break;
+      case 3: grid = launch<3>(a, stream, nsm, m32); break;
+      case 4: grid = launch<4>(a, stream, nsm, m32); break;
+      default: grid = launch<8>(a, stream, nsm, m32); break;
     }
     if (static_cast<size_t>(grid) * kWarps > nw_max) fail(XE_ERR_ARG, "evaluator scratch too small");
   }

@@ -69,6 +69,38 @@ __global__ void col_norm_kernel(const int64_t* cp, const int32_t* row, const dou
   }
 }
 
+// 1 / inf-norm of each row of K (1 for empty rows): the rows are normalised
+// before Ruiz, so the equilibration starts from unit-scale rows whatever the
+// units (bytes in EQ13/EQ14, h_max in EQ16, q in the energy rows)
+__global__ void row_inf_kernel(const int64_t* rp, const double* val, int64_t m, double* out) {
+  GRID_LOOP(i, m) {
+    double s = 0.0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s = fmax(s, fabs(val[k]));
+    out[i] = s > 0.0 ? 1.0 / s : 1.0;
+  }
+}
+
+// Presolve of the prohibitive-cost columns (cost >= 1e9, lower bound 0):
+// fixed at 0 with zero cost in the solved problem.
+__global__ void sentinel_kernel(const double* c, const double* lb, const double* ub, int64_t n, double* c_out,
+                                double* ub_out, unsigned long long* count) {
+  GRID_LOOP(j, n) {
+    const bool fix = c[j] >= 1.0e9 && lb[j] <= 0.0;
+    c_out[j] = fix ? 0.0 : c[j];
+    ub_out[j] = fix ? 0.0 : ub[j];
+    if (fix) atomicAdd(count, 1ull);
+  }
+}
+
+// Certificate for the presolve: reduced cost of every fixed column under the
+// final duals, c_j - (K'y)_j with (K'y)_j = (K~'y~)_j / Dc_j, must be >= 0.
+__global__ void certify_kernel(const double* c, const double* lb, const double* Kty_s, const double* Dc, int64_t n,
+                               unsigned long long* bad) {
+  GRID_LOOP(j, n) {
+    if (c[j] >= 1.0e9 && lb[j] <= 0.0 && c[j] - Kty_s[j] / Dc[j] < 0.0) atomicAdd(bad, 1ull);
+  }
+}
+
 __global__ void rescale_kernel(double* D, const double* nrm, int64_t n) {
   GRID_LOOP(i, n) {
     const double v = nrm[i];
@@ -163,7 +195,7 @@ __global__ void dual_kernel(Iter it) {
 // partial sums for the KKT measures, 8 doubles per block:
 // [primal obj, primal viol^2 (unscaled), dual row obj, dual bound obj, |b|^2, |c|^2, -, -]
 __global__ void kkt_rows_kernel(const double* Kx, const double* b, const int8_t* sense, const double* y,
-                                const double* Dr, int64_t m, double* part) {
+                                const double* Dr, const double* Dr0, int64_t m, double* part) {
   __shared__ double sh[2][kB];
   double v2 = 0.0, dobj = 0.0;
   GRID_LOOP(i, m) {
@@ -173,7 +205,7 @@ __global__ void kkt_rows_kernel(const double* Kx, const double* b, const int8_t*
     if (sn == 'E') viol = r;
     else if (sn == 'G') viol = fmin(r, 0.0);
     else viol = fmax(r, 0.0);
-    viol /= Dr[i];
+    viol = viol / Dr[i] * Dr0[i];  // residual of the row-normalised problem
     v2 += viol * viol;
     dobj += b[i] * y[i];
   }
@@ -255,7 +287,7 @@ __global__ void normalize_kernel(double* v, const double* part, int nb, int64_t 
 using namespace pd;
 
 struct PdhgState {
-  DevBuf<double> Dr, Dc, val_s, cval_s, c_s, lb_s, ub_s, b_s, x, xbar, xsum, y, ysum, xr, yr, Kx, Kty, xa, ya, part,
+  DevBuf<double> Dr, Dr0, Dc, c_fix, ub_fix, val_s, cval_s, c_s, lb_s, ub_s, b_s, x, xbar, xsum, y, ysum, xr, yr, Kx, Kty, xa, ya, part,
       step, tmpn, tmpm;
   DevBuf<int32_t> col_of;
 };
@@ -267,7 +299,10 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   const int64_t m = M->info.n_rows, n = M->info.n_cols, nnz = M->info.nnz;
   PdhgState S;
   S.Dr.alloc(m);
+  S.Dr0.alloc(m);
   S.Dc.alloc(n);
+  S.c_fix.alloc(n);
+  S.ub_fix.alloc(n);
   S.val_s.alloc(nnz);
   S.cval_s.alloc(nnz);
   S.c_s.alloc(n);
@@ -293,6 +328,9 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
     ub = ub_o.p;
   }
 
+  DevBuf<unsigned long long> fixcnt;
+  fixcnt.alloc(2);
+  XE_CUDA(cudaMemsetAsync(fixcnt.p, 0, 16, s));
   cudaEvent_t e0, e1;
   XE_CUDA(cudaEventCreate(&e0));
   XE_CUDA(cudaEventCreate(&e1));
@@ -300,8 +338,9 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
 
   // ---- preconditioning: Ruiz (inf-norm) x10, then Pock-Chambolle (l1)
   {
-    std::vector<double> ones_m(static_cast<size_t>(m), 1.0), ones_n(static_cast<size_t>(n), 1.0);
-    XE_CUDA(cudaMemcpyAsync(S.Dr.p, ones_m.data(), m * 8, cudaMemcpyHostToDevice, s));
+    std::vector<double> ones_n(static_cast<size_t>(n), 1.0);
+    row_inf_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->val.p, m, S.Dr0.p);
+    XE_CUDA(cudaMemcpyAsync(S.Dr.p, S.Dr0.p, m * 8, cudaMemcpyDeviceToDevice, s));
     XE_CUDA(cudaMemcpyAsync(S.Dc.p, ones_n.data(), n * 8, cudaMemcpyHostToDevice, s));
     for (int it = 0; it < 11; ++it) {
       const int p = it == 10 ? 1 : 0;
@@ -312,7 +351,8 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
     }
     scale_csr_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->col.p, M->val.p, S.Dr.p, S.Dc.p, m, S.val_s.p);
     scale_csc_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, M->cval.p, S.Dr.p, S.Dc.p, n, S.cval_s.p);
-    scale_vec_kernel<<<grid(n), kB, 0, s>>>(M->obj.p, lb, ub, S.Dc.p, n, S.c_s.p, S.lb_s.p, S.ub_s.p);
+    sentinel_kernel<<<grid(n), kB, 0, s>>>(M->obj.p, lb, ub, n, S.c_fix.p, S.ub_fix.p, fixcnt.p);
+    scale_vec_kernel<<<grid(n), kB, 0, s>>>(S.c_fix.p, lb, S.ub_fix.p, S.Dc.p, n, S.c_s.p, S.lb_s.p, S.ub_s.p);
     scale_b_kernel<<<grid(m), kB, 0, s>>>(M->rhs.p, S.Dr.p, m, S.b_s.p);
     XE_CUDA(cudaGetLastError());
   }
@@ -403,11 +443,12 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   struct Kkt {
     double gap, pres, pobj, dobj, err;
   };
-  std::vector<double> hb(static_cast<size_t>(m));
+  std::vector<double> hb(static_cast<size_t>(m)), hd0(static_cast<size_t>(m));
   XE_CUDA(cudaMemcpyAsync(hb.data(), M->rhs.p, m * 8, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaMemcpyAsync(hd0.data(), S.Dr0.p, m * 8, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaStreamSynchronize(s));
   double b_l2 = 0.0;
-  for (double v : hb) b_l2 += v * v;
+  for (size_t i = 0; i < hb.size(); ++i) b_l2 += (hb[i] * hd0[i]) * (hb[i] * hd0[i]);
   b_l2 = std::sqrt(b_l2);
 
   auto kkt = [&](const double* xs, const double* ys) {
@@ -415,7 +456,7 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
     spmtv_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, S.cval_s.p, ys, n, S.Kty.p);
     const int gm = grid(m), gn = grid(n), g = std::max(gm, gn);
     XE_CUDA(cudaMemsetAsync(S.part.p, 0, static_cast<size_t>(g) * 4 * 8, s));
-    kkt_rows_kernel<<<gm, kB, 0, s>>>(S.Kx.p, S.b_s.p, M->sense.p, ys, S.Dr.p, m, S.part.p);
+    kkt_rows_kernel<<<gm, kB, 0, s>>>(S.Kx.p, S.b_s.p, M->sense.p, ys, S.Dr.p, S.Dr0.p, m, S.part.p);
     kkt_cols_kernel<<<gn, kB, 0, s>>>(xs, S.c_s.p, S.lb_s.p, S.ub_s.p, S.Kty.p, n, S.part.p);
     std::vector<double> h(static_cast<size_t>(g) * 4);
     XE_CUDA(cudaMemcpyAsync(h.data(), S.part.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -508,6 +549,14 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   cudaGraphExecDestroy(gexec);
   cudaGraphDestroy(graph);
 
+  // certify the prohibitive-cost presolve with the final duals
+  spmtv_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, S.cval_s.p, S.y.p, n, S.Kty.p);
+  certify_kernel<<<grid(n), kB, 0, s>>>(M->obj.p, lb, S.Kty.p, S.Dc.p, n, fixcnt.p + 1);
+  unsigned long long fc[2] = {0, 0};
+  XE_CUDA(cudaMemcpyAsync(fc, fixcnt.p, 16, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaStreamSynchronize(s));
+  res->presolve_fixed = static_cast<int32_t>(fc[0]);
+  res->certified = fc[1] == 0 ? 1 : 0;
   res->primal_obj = cur.pobj;
   res->dual_obj = cur.dobj;
   res->rel_gap = cur.gap;
