@@ -119,6 +119,7 @@ def main():
     ap.add_argument("--e2e-n", type=int, default=2_000_000, help="candidates per e2e step")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-pdhg", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -256,6 +257,28 @@ def main():
                        "h2d_bytes_per_step": ne * cube_bytes, "d2h_bytes_per_step": 24 * ((ne + (1 << 20) - 1) // (1 << 20)),
                        "candidates_per_step": ne, "path": "xe_eval_cubes_host (canonical cubes in a pinned host buffer; 2-stream chunked H2D, on-device transpose, lane-per-candidate evaluator)"}
         assert re.best_index == -1 or re.best_index < ne
+
+    # ---- K1 + K3 on the same config: GPU model assembly, PDHG LP relaxation ----
+    if rank == 0 and not args.skip_pdhg:
+        hbm_gbs = peaks()[0]
+        model = xe.build_model(prob)
+        build_ms = model.build_ms()
+        k1_bytes = 12 * model.nnz + 8 * (model.n_rows + 1) + 26 * model.n_cols
+        lp = xe.pdhg_solve(model, tol=1e-7, max_iters=400000)
+        want = 118.68224203657523  # HiGHS 1.12.0 on the reference MPS (tests/golden/lp_values.json)
+        it_bytes = 24 * model.nnz + 56 * (model.n_rows + model.n_cols)
+        line["k1_build"] = {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "ms": build_ms,
+                            "achieved_gbs": k1_bytes / (build_ms / 1e3) / 1e9 if build_ms > 0 else None}
+        line["pdhg"] = {
+            "metric": "PDHG iters/sec", "workload": "vgg16 cfg2 LP relaxation (K1 model, binaries in [0,1])",
+            "iters": lp.iters, "restarts": lp.restarts, "converged": lp.converged, "certified": lp.certified,
+            "iters_per_s": lp.iters / (lp.solve_ms / 1e3) if lp.solve_ms > 0 else None,
+            "time_to_tol_ms": lp.solve_ms, "tol": 1e-7, "objective": lp.primal_obj, "highs_objective": want,
+            "rel_err": abs(lp.primal_obj - want) / want,
+            "roofline": {"bound": "hbm", "bytes_per_iter": it_bytes,
+                         "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9 if lp.ms_per_iter > 0 else None,
+                         "peak": hbm_gbs, "unit": "GB/s"},
+        }
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     if rank == 0 and world == 1 and not args.skip_cpu:

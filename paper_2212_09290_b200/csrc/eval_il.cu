@@ -169,7 +169,7 @@ __device__ __noinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t*
 // M: integer type of tensor masses and memory sums (int32 when twice the
 // save-all total fits, halving the table traffic; int64 otherwise).
 template <int MAXD, class M>
-__global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 4 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NW = 1;
   const DevProblem& P = a.P;
