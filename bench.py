@@ -30,6 +30,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 METRIC = "candidate schedules evaluated/sec + PDHG iters/sec at 1/2/4/8 B200 vs CPU ref"
 UNIT = "candidates/s"
 SEED = 2212
+WORKLOAD = "vgg16-train cfg2 dense R/S candidate evaluation (T=43, E=63, D=2, gpu budget 25%)"
 
 
 def peaks():
@@ -99,8 +100,7 @@ def reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
         "data": "synthetic (bench/configs.py vgg16_doc; tests/cubegen.py mixed candidates, seed 2212)",
-        "config": {"workload": "vgg16-train cfg2 dense R/S candidate evaluation (T=43, D=2, gpu 25%)",
-                   "sample_per_step": int(np.mean(counts))},
+        "config": {"workload": WORKLOAD, "sample_per_step": int(np.mean(counts))},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
                          "sample": f"{int(np.mean(counts))} VGG-16 candidates per step, "
                                    "complete_assignment+objective_value+check_assignment+peaks"},
@@ -217,7 +217,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+u32",
         "data": "synthetic: K4 round_cubes (placement + minimal-save + <=3 recompute edits + 10% bit flips), Philox seed 2212",
-        "config": {"workload": "vgg16-train cfg2 dense R/S candidate evaluation (T=43, E=63, D=2, gpu budget 25%)",
+        "config": {"workload": WORKLOAD,
                    "candidates_per_gpu": n, "cube_bytes": cube_bytes, "resident_bytes_per_gpu": n * cube_bytes,
                    "l2": "inputs (13.8 GB) larger than L2 (126 MB); no flush needed",
                    "layout": "xe_cube_il (candidate-interleaved, 32-candidate groups)",
