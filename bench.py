@@ -41,11 +41,14 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def traffic_from_profiles(config):
+def traffic_from_profiles(config, n):
+    """DRAM bytes (read + write) per launch of n candidates, scaled from the
+    per-candidate traffic of the committed ncu --set full capture; GB."""
     p = os.path.join(ROOT, "profiles", "k2a_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d.get(config)
+        d = json.load(open(p)).get(config)
+        if d:
+            return d["dram_bytes_per_candidate"] * n / 1e9
     return None
 
 
@@ -224,7 +227,8 @@ def main():
                    "parallelism": f"dp{world} (candidate shards, NCCL all-reduce MIN incumbent)"},
         "best": {"obj_ms": best_obj, "index": best_idx, "n_valid_rank0": r.n_valid},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic_from_profiles("vgg16"),
+                     "frac": achieved / hbm, "traffic": traffic_from_profiles("vgg16", n), "traffic_unit": "GB per launch",
+                     "algorithmic_gb_per_launch": n * bytes_per_cand / 1e9,
                      "peak_kind": peak_kind, "kernel_ms": kern_ms,
                      "bytes_per_candidate": bytes_per_cand},
         "clocks": clocks,

@@ -43,6 +43,10 @@ using cube::row_peak_general;
 using cube::TState;
 
 constexpr int kWarps = 8;
+// fixed shared-memory prefix (T <= 64): byte tables [8][256], masses [64],
+// parent / consumer masks [64]
+constexpr int kOffMtab = 0, kOffMass = 8 * 256 * 8, kOffPmask = kOffMass + 64 * 8, kOffCons = kOffPmask + 64 * 8,
+              kFixed = kOffCons + 64 * 8;
 
 struct IlArgs {
   DevProblem P;
@@ -176,10 +180,11 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
   const int D = cube::ndev<MAXD>(P), T = P.T, E = P.E;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
-  M* s_mass = reinterpret_cast<M*>(smem + a.off_mass);
-  uint64_t* s_pmask = reinterpret_cast<uint64_t*>(smem + a.off_pmask);
-  uint64_t* s_cons = reinterpret_cast<uint64_t*>(smem + a.off_cons);
-  M* s_mtab = reinterpret_cast<M*>(smem + a.off_mtab);
+  // the hottest tables sit at compile-time offsets (immediate LDS offsets)
+  M* s_mass = reinterpret_cast<M*>(smem + kOffMass);
+  uint64_t* s_pmask = reinterpret_cast<uint64_t*>(smem + kOffPmask);
+  uint64_t* s_cons = reinterpret_cast<uint64_t*>(smem + kOffCons);
+  M* s_mtab = reinterpret_cast<M*>(smem + kOffMtab);
   double* s_tab = reinterpret_cast<double*>(smem + a.off_tab);
   int32_t* s_inptr = reinterpret_cast<int32_t*>(smem + a.off_inptr);
   int32_t* s_inedge = reinterpret_cast<int32_t*>(smem + a.off_inedge);
@@ -597,7 +602,7 @@ void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint6
   a.strict = opts.strict_free ? 1 : 0;
   a.energy = (opts.use_energy && h.has_energy) ? 1 : 0;
   a.valid_mask = valid_mask;
-  int off = 0;
+  int off = kFixed;
   auto take = [&](int bytes) {
     int o = off;
     off = align16(off + bytes);
@@ -610,10 +615,10 @@ void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint6
   const bool m32 = total_mass < (int64_t{1} << 30);
   const int msz = m32 ? 4 : 8;
   const int n_dt = P.D * P.T, n_copy = P.E * P.D * P.D;
-  a.off_mass = take(msz * P.T);
-  a.off_pmask = take(8 * P.T);
-  a.off_cons = take(8 * P.T);
-  a.off_mtab = take(msz * 256 * P.NB);
+  a.off_mass = kOffMass;
+  a.off_pmask = kOffPmask;
+  a.off_cons = kOffCons;
+  a.off_mtab = kOffMtab;
   a.off_inptr = take(4 * (P.T + 1));
   a.off_inedge = take(4 * std::max(1, P.E));
   a.off_src = take(4 * std::max(1, P.E));
