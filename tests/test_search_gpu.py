@@ -1,0 +1,64 @@
+# SPDX-License-Identifier: Apache-2.0
+"""K1 -> K3 -> K4 -> K2 search reproduces the reference's exact optima on
+config 1 (the reference's own pins, proj/tests/test_solver.cpp):
+  F1 chain3 9.0 (:66-86), 8 MiB -> 9.0, 3 MiB infeasible (:88-97),
+  F2 fig2 11.0 (:99-119),
+  F3 chain_lowmem sweep 24, 24, 24, 24, 27 at 100/65/50/35/25 % and
+  10 MiB -> 24, 9/8 MiB -> 27, 4 MiB - 1 infeasible (:121-153)."""
+import numpy as np
+import pytest
+
+from conftest import golden_problem_text
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_2212_09290_b200 as xe  # noqa: E402
+from paper_2212_09290_b200.search import search  # noqa: E402
+
+MiB = 1 << 20
+
+
+def prob(name, budget=None):
+    p = xe.Problem.from_json(golden_problem_text(name))
+    return p if budget is None else p.with_budgets([budget] * p.D)
+
+
+def check(p, r, want):
+    assert r.objective == want, (r.objective, want, r.n_valid)
+    b = p.arrays()["budget_bytes"]
+    assert (r.peaks <= b).all()
+    assert r.lp_bound is None or r.lp_bound <= want + 1e-6
+
+
+def test_chain3():
+    p = prob("chain3")
+    check(p, search(p, n_per_round=1 << 14, rounds=2), 9.0)
+    p8 = prob("chain3", 8 * MiB)
+    check(p8, search(p8, n_per_round=1 << 14, rounds=2), 9.0)
+    r3 = search(prob("chain3", 3 * MiB), n_per_round=1 << 14, rounds=2, use_lp=False)
+    assert r3.index == -1 and r3.n_valid == 0
+
+
+def test_fig2():
+    p = prob("fig2")
+    r = search(p, n_per_round=1 << 16, rounds=2)
+    check(p, r, 11.0)
+    assert r.lp_certified
+
+
+@pytest.mark.parametrize("pct,want", [(100, 24.0), (65, 24.0), (50, 24.0), (35, 24.0), (25, 27.0)])
+def test_chain_lowmem_sweep(pct, want):
+    full = 34 * MiB
+    p = prob("chain_lowmem", full * pct // 100)
+    check(p, search(p, n_per_round=1 << 17, rounds=4), want)
+
+
+@pytest.mark.parametrize("budget,want", [(10 * MiB, 24.0), (9 * MiB, 27.0), (8 * MiB, 27.0)])
+def test_chain_lowmem_boundaries(budget, want):
+    p = prob("chain_lowmem", budget)
+    check(p, search(p, n_per_round=1 << 17, rounds=4), want)
+
+
+def test_chain_lowmem_infeasible_below_largest_tensor():
+    r = search(prob("chain_lowmem", 4 * MiB - 1), n_per_round=1 << 14, rounds=1, use_lp=False)
+    assert r.index == -1
