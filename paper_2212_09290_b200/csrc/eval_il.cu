@@ -140,7 +140,7 @@ __device__ __noinline__ uint32_t eq11_flags(const uint64_t* R, const uint64_t* S
 // device holding the parent u; illegal when that device freed u at an
 // earlier step of timestep t (schedule.cpp:52-71).
 template <int MAXD>
-__device__ __noinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t* S, const uint64_t* Sn,
+__device__ __forceinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t* S, const uint64_t* Sn,
                                               const uint64_t* needD, uint64_t rany, int t, int D, int strict,
                                               const uint64_t* s_cons) {
   uint64_t zany = 0;
@@ -172,7 +172,10 @@ __device__ __noinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t*
 
 // M: integer type of tensor masses and memory sums (int32 when twice the
 // save-all total fits, halving the table traffic; int64 otherwise).
-template <int MAXD, class M>
+// NBYTES: bytes of a bit row summed through the byte tables (4 for T <= 32,
+// else 8; tables beyond the problem's bytes are zero), so every lookup is
+// unconditional.
+template <int MAXD, class M, int NBYTES>
 __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int NW = 1;
@@ -201,7 +204,8 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
     s_pmask[i] = P.pmask[i];
     s_cons[i] = P.cons[i];
   }
-  for (int i = threadIdx.x; i < P.NB * 256; i += blockDim.x) s_mtab[i] = static_cast<M>(P.mtab[i]);
+  for (int i = threadIdx.x; i < NBYTES * 256; i += blockDim.x)
+    s_mtab[i] = i < P.NB * 256 ? static_cast<M>(P.mtab[i]) : M(0);
   for (int i = threadIdx.x; i < n_dt; i += blockDim.x) {
     s_tab[i] = P.table[i];
     if (a.energy) s_tab[n_dt + i] = P.table[n_dt + n_copy + i];
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
   M* s_pk = reinterpret_cast<M*>(queue + a.q_cap);  // [32][MAXD] deferred row peaks
   for (int i = lane; i < 32 * MAXD; i += 32) s_pk[i] = 0;
   __syncthreads();
-  const double* copy_tab = a.copy_in_smem ? s_copy : P.table + n_dt;
+  const double* copy_glob = P.table + n_dt;  // copy terms in global memory (large E*D*D)
   int q_cnt = 0;  // warp-uniform
   auto drain = [&]() {
     __syncwarp();
@@ -343,8 +347,7 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
           M base = 0;
           const uint32_t lo = static_cast<uint32_t>(S[d]), hi = static_cast<uint32_t>(S[d] >> 32);
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (b < P.NB) base += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+          for (int b = 0; b < NBYTES; ++b) base += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
           const uint64_t r = R[d];
           const bool multi = (r & (r - 1)) != 0;
           const unsigned ballot = __ballot_sync(0xffffffffu, multi);
@@ -404,8 +407,10 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
               if (dc >= D || !((R[dc] >> v) & 1ull)) continue;
 #pragma unroll
               for (int ds = 0; ds < MAXD; ++ds)
-                if (ds < D && ds != dc && (((R[ds] | S[ds]) >> u) & 1ull))
-                  total = __dadd_rn(total, copy_tab[(e * D + ds) * D + dc]);
+                if (ds < D && ds != dc && (((R[ds] | S[ds]) >> u) & 1ull)) {
+                  const int idx = (e * D + ds) * D + dc;
+                  total = __dadd_rn(total, a.copy_in_smem ? s_copy[idx] : __ldg(copy_glob + idx));
+                }
             }
           }
         };
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
             st.Z[d].w[0] = R[d] | S[d];
           }
           for_copy_terms<NW, MAXD, true>(st, P, s_inptr, s_inedge, s_src, s_dst, [&](int idx) {
-            total = __dadd_rn(total, copy_tab[idx - n_dt]);
+            total = __dadd_rn(total, a.copy_in_smem ? s_copy[idx - n_dt] : __ldg(copy_glob + idx - n_dt));
           });
         }
         // ---- ENERGY_TOTAL row of timestep t: sequential (d, i) sum
@@ -545,7 +550,7 @@ int align16(int x) { return (x + 15) & ~15; }
 
 template <int MAXD, class M>
 int launch_m(const IlArgs& a, cudaStream_t s, int nsm) {
-  auto k = eval_il_kernel<MAXD, M>;
+  auto k = a.P.T <= 32 ? eval_il_kernel<MAXD, M, 4> : eval_il_kernel<MAXD, M, 8>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes));
   int per_sm = 0;
   XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarps * 32, a.smem_bytes));

@@ -15,7 +15,9 @@
 //   2. minimal-save S: S(dev_i, t, i) = 1 for i < t <= last consumer of i;
 //   3. up to `edits` drop-and-recompute edits: the tensor of op i is dropped
 //      over a window before one of its consumers and recomputed there
-//      (possibly on another device), parents' saves extended as needed;
+//      (possibly on another device); each parent not resident at that step
+//      is either kept saved until then or itself recomputed there (dropping
+//      its own save window), recursively — chains of recomputation;
 //   4. with probability `perturb`, one uniformly random R/S bit is flipped.
 // One warp per candidate; the cube is assembled in shared memory and written
 // out with coalesced 16-byte stores.
@@ -171,27 +173,57 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
           }
         if (a0 > t) continue;
         const int a1 = a0 + rng.below(t - a0 + 1);
-        const int di = dev[i];
         int dn = rng.uniform() < 0.5 ? rng.below(D) : dev[t];
-        if (a.cost[dn * T + i] >= 1.0e9) dn = di;
-        for (int tt = a1; tt <= t; ++tt) bit_clr(1, di, tt, i);
-        bit_set(0, dn, t, i);
-        if (dn != di)
-          for (int tt = t + 1; tt < T; ++tt)
-            if (bit_get(1, di, tt, i)) {
-              bit_clr(1, di, tt, i);
-              bit_set(1, dn, tt, i);
+        if (a.cost[dn * T + i] >= 1.0e9) dn = dev[i];
+        // recompute op v at t on dn, dropping its saves on dev-of-v over
+        // [from, t]; later saves follow it to dn (EQ11 needs a holder at t)
+        auto recompute_at = [&](int v, int from) {
+          const int dv = dev[v];
+          for (int tt = from; tt <= t; ++tt) bit_clr(1, dv, tt, v);
+          bit_set(0, dn, t, v);
+          if (dn != dv)
+            for (int tt = t + 1; tt < T; ++tt)
+              if (bit_get(1, dv, tt, v)) {
+                bit_clr(1, dv, tt, v);
+                bit_set(1, dn, tt, v);
+              }
+        };
+        recompute_at(i, a1);
+        // parents of every op recomputed at t: keep them saved until t, or
+        // (probability 1/2, when dn can run them) recompute them at t too,
+        // dropping their own save windows — chains of recomputation
+        int stack[32], sp = 0;
+        stack[sp++] = i;
+        while (sp > 0) {
+          const int v = stack[--sp];
+          for (int k2 = a.in_ptr[v]; k2 < a.in_ptr[v + 1]; ++k2) {
+            const int p = a.src[a.in_edge[k2]];
+            bool avail = false;
+            for (int d = 0; d < D; ++d) avail |= bit_get(0, d, t, p) || bit_get(1, d, t, p);
+            if (avail) continue;
+            if (sp < 32 && a.cost[dn * T + p] < 1.0e9 && rng.uniform() < 0.5) {
+              // first step after p's last use before t
+              int from = p + 1;
+              for (int tt = t - 1; tt > p && from == p + 1; --tt)
+                for (int e = 0; e < a.E; ++e) {
+                  if (a.src[e] != p) continue;
+                  bool used = false;
+                  for (int d = 0; d < D; ++d) used |= bit_get(0, d, tt, a.dst[e]);
+                  if (used) {
+                    from = tt + 1;
+                    break;
+                  }
+                }
+              recompute_at(p, from);
+              stack[sp++] = p;
+              continue;
             }
-        for (int k2 = a.in_ptr[i]; k2 < a.in_ptr[i + 1]; ++k2) {
-          const int p = a.src[a.in_edge[k2]];
-          bool avail = false;
-          for (int d = 0; d < D; ++d) avail |= bit_get(0, d, t, p) || bit_get(1, d, t, p);
-          if (avail) continue;
-          const int dp = dev[p];
-          int ls = p;
-          for (int tt = p + 1; tt <= t; ++tt)
-            if (bit_get(1, dp, tt, p)) ls = tt;
-          for (int tt = ls + 1; tt <= t; ++tt) bit_set(1, dp, tt, p);
+            const int dp = dev[p];
+            int ls = p;
+            for (int tt = p + 1; tt <= t; ++tt)
+              if (bit_get(1, dp, tt, p)) ls = tt;
+            for (int tt = ls + 1; tt <= t; ++tt) bit_set(1, dp, tt, p);
+          }
         }
       }
       // 4. perturbation

@@ -45,8 +45,17 @@ class SearchResult:
 
 def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: int = 1 << 18,
            rounds: int = 4, seed: int = 1, edits: int = 3, use_lp: bool = True,
-           valid_mask: int = DEFAULT_MASK, first: int = 0, lp_tol: float = 1e-6) -> SearchResult:
+           valid_mask: int = DEFAULT_MASK, first: int = 0, lp_tol: float = 1e-6,
+           distributed: bool = False) -> SearchResult:
+    """distributed=True (torch.distributed initialised, one process per GPU):
+    rank r evaluates global index blocks (round * world + r) * n_per_round,
+    the incumbent is exchanged with shard.exchange_best; every rank returns
+    the global result (the LP is solved on every rank: PDHG is deterministic)."""
     import torch
+    rank, world = 0, 1
+    if distributed:
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
     opts = opts or ModelOptions()
     x_dev, lp_val, cert = None, None, True
     if use_lp:
@@ -56,13 +65,17 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
         lp_val, cert = lp.primal_obj, lp.certified
     best_obj, best_idx, n_valid = float("inf"), -1, 0
     for r in range(rounds):
-        lo = first + r * n_per_round
+        lo = first + (r * world + rank) * n_per_round
         cubes = round_cubes(problem, n_per_round, seed, first=lo, edits=edits, perturb=0.0, x=x_dev)
         res = evaluate_cubes(problem, cubes, opts, valid_mask=valid_mask, outputs=False)
         n_valid += res.n_valid
         if res.best_index >= 0 and res.best_obj < best_obj:  # rounds ascend in index: strict <
             best_obj, best_idx = res.best_obj, lo + res.best_index
         del cubes
+    if world > 1:
+        from .shard import exchange_best
+        inc = exchange_best(best_obj, best_idx, n_valid, offset=0, device="cuda")
+        best_obj, best_idx, n_valid = inc.obj, inc.index, inc.n_valid
     cube = peaks = None
     if best_idx >= 0:
         c = round_cubes(problem, 1, seed, first=best_idx, edits=edits, perturb=0.0, x=x_dev)
@@ -70,4 +83,4 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
         assert r1.best_obj == best_obj, (r1.best_obj, best_obj)
         cube = c.cpu().numpy().view(np.uint32)[0]
         peaks = r1.peak.cpu().numpy()[0]
-    return SearchResult(best_obj, best_idx, cube, peaks, lp_val, cert, rounds * n_per_round, n_valid)
+    return SearchResult(best_obj, best_idx, cube, peaks, lp_val, cert, rounds * n_per_round * world, n_valid)
