@@ -270,46 +270,30 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
       for (int d = 0; d < D; ++d) {
         const uint64_t ebad = a.energy ? s_ebad[d] : 0ull;
         const double* ct = s_tab + d * T;
+        // one R row of pass B: the first set bit is handled without a branch
+        // (an empty row adds +0.0: the running total is never negative, so
+        // that is the identity); further bits (recomputations) loop
+        auto row_b = [&](uint64_t r, int tt) {
+          const uint64_t above = tt >= 63 ? 0ull : (~0ull << (tt + 1));
+          if (r & above) fl |= XE_F_FIXED_ZERO;
+          const uint64_t on = (r >> tt) & 1ull;
+          eq9 += static_cast<int>(on);
+          multi |= diag & (on << tt);
+          diag |= on << tt;
+          if (r & ebad) fl |= XE_F_ENERGY_DEV;
+          const double v0 = ct[r ? __ffsll(r) - 1 : 0];
+          total = __dadd_rn(total, r ? v0 : 0.0);
+          for (r &= r - 1; r; r &= r - 1) total = __dadd_rn(total, ct[__ffsll(r) - 1]);
+        };
         int t = 0;
         for (; t + 4 <= T; t += 4) {
           uint64_t r4[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) r4[j] = ldR(d, t + j);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint64_t r = r4[j];
-            const int tt = t + j;
-            const uint64_t above = tt >= 63 ? 0ull : (~0ull << (tt + 1));
-            if (r & above) fl |= XE_F_FIXED_ZERO;
-            if ((r >> tt) & 1ull) {
-              ++eq9;
-              multi |= diag & (1ull << tt);
-              diag |= 1ull << tt;
-            }
-            if (r & ebad) fl |= XE_F_ENERGY_DEV;
-            while (r) {
-              const int i = __ffsll(r) - 1;
-              r &= r - 1;
-              total = __dadd_rn(total, ct[i]);
-            }
-          }
+          for (int j = 0; j < 4; ++j) row_b(r4[j], t + j);
         }
-        for (; t < T; ++t) {
-          uint64_t r = ldR(d, t);
-          const uint64_t above = t >= 63 ? 0ull : (~0ull << (t + 1));
-          if (r & above) fl |= XE_F_FIXED_ZERO;
-          if ((r >> t) & 1ull) {
-            ++eq9;
-            multi |= diag & (1ull << t);
-            diag |= 1ull << t;
-          }
-          if (r & ebad) fl |= XE_F_ENERGY_DEV;
-          while (r) {
-            const int i = __ffsll(r) - 1;
-            r &= r - 1;
-            total = __dadd_rn(total, ct[i]);
-          }
-        }
+        for (; t < T; ++t) row_b(ldR(d, t), t);
       }
       if (diag != valid || multi) fl |= XE_F_EQ8;
       if (eq9 != T) fl |= XE_F_EQ9;
