@@ -112,6 +112,71 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def placement_sweep(args):
+    """BASELINE config 5: synthetic 2000-op random DAG, 8 devices; K2b
+    evaluates save-all placements (save_all_assignment + objective_value,
+    solver.cpp:30-75) generated uniformly (xe_random_placements); one step =
+    one batch of n placements resident in HBM.  The full 1B sweep is
+    ceil(1e9 / n) such steps."""
+    import torch
+    import torch.distributed as dist
+    import paper_2212_09290_b200 as xe
+    from bench import configs
+    from bench.clocks import ClockSampler
+    from paper_2212_09290_b200.shard import exchange_best
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prob = xe.Problem.from_json(configs.random2000_doc(), device=local)
+    n = min(args.n, 4_000_000)
+    dev = xe.random_placements(prob, n, SEED, first=rank * n)
+    out = (torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty((n, prob.D), dtype=torch.int64, device="cuda"),
+           torch.empty(n, dtype=torch.int32, device="cuda"))
+    stream = torch.cuda.current_stream()
+    step = lambda: xe.evaluate_placements(prob, dev, policy=0, out=out, stream=stream.cuda_stream)
+    for _ in range(args.warmup):
+        r = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    best_obj, best_idx = r.best_obj, r.best_index
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        inc = exchange_best(best_obj, best_idx, r.n_valid, offset=rank * n, device="cuda")
+        best_obj, best_idx = inc.obj, inc.index
+    ms = float(t[0])
+    bpc = prob.T + 8 + 8 * prob.D + 4
+    hbm = peaks()[0]
+    achieved = n * bpc / (ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": world * n / (ms / 1e3), "unit": "placements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+u8",
+            "data": "synthetic: xe_random_placements (uniform over allowed devices), Philox seed 2212",
+            "config": {"workload": "random 2000-op DAG cfg5 save-all placement sweep (T=2000, E=5987, D=8)",
+                       "placements_per_gpu_step": n, "sweep_1e9_seconds": 1e9 / (world * n / (ms / 1e3)),
+                       "parallelism": f"dp{world}"},
+            "best": {"obj_ms": best_obj, "index": best_idx},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "bytes_per_candidate": bpc},
+            "clocks": clk.summary(), "gpu_launches": 2 * args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -123,10 +188,14 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-pdhg", action="store_true")
+    ap.add_argument("--workload", default="vgg16", choices=["vgg16", "random2000"],
+                    help="vgg16: BASELINE config 2 (the headline); random2000: config 5 placement sweep")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return reference_arm(args)
+    if args.workload == "random2000":
+        return placement_sweep(args)
 
     import torch
     import torch.distributed as dist

@@ -304,6 +304,11 @@ int xe_pdhg_solve(xe_csr* m, const xe_pdhg_opts* opts, xe_pdhg_result* res,
 int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int64_t first,
                    int64_t n, int32_t edits, double perturb, uint32_t* cubes_dev,
                    void* stream);
+/* n uniform random placements dev[n][T] (device buffer): op i on a device
+ * that can run it (cost < 1e9), candidate k a pure function of
+ * (seed, first + k) — the input family of config 5's placement sweep. */
+int xe_random_placements(const xe_problem* p, uint64_t seed, int64_t first, int64_t n, uint8_t* dev_out,
+                         void* stream);
 
 #ifdef __cplusplus
 }

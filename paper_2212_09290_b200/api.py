@@ -218,6 +218,48 @@ def evaluate_cubes_il(problem: Problem, il, n: int, opts: Optional[ModelOptions]
     return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
 
 
+def random_placements(problem: Problem, n: int, seed: int, first: int = 0, out=None, stream=None):
+    """n uniform random placements (uint8 CUDA tensor [n, T]); candidate k is
+    a pure function of (seed, first + k)."""
+    import torch
+    if out is None:
+        out = torch.empty((n, problem.T), dtype=torch.uint8, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.xe_random_placements(problem.handle, seed, first, n, C.c_void_p(out.data_ptr()), C.c_void_p(s)))
+    return out
+
+
+def evaluate_placements(problem: Problem, dev, policy: int = 0, valid_mask: int = _lib.F_CHECK_MASK,
+                        outputs: bool = True, stream=None, out=None, best: bool = True):
+    """K2b: device placements (uint8 CUDA tensor [n, T]); policy 0 = save-all
+    (save_all_assignment, solver.cpp:30-42), 1 = minimal-save."""
+    import torch
+    n = dev.shape[0]
+    if out is not None:
+        obj, peak, flags = out
+    else:
+        obj = torch.empty(n, dtype=torch.float64, device=dev.device) if outputs else None
+        peak = torch.empty((n, problem.D), dtype=torch.int64, device=dev.device) if outputs else None
+        flags = torch.empty(n, dtype=torch.int32, device=dev.device) if outputs else None
+    eo = _lib.EvalOut(_ptr(obj), _ptr(peak), _ptr(flags))
+    b = _lib.Best()
+    s = stream if stream is not None else torch.cuda.current_stream(dev.device).cuda_stream
+    check(LIB.xe_eval_placements(problem.handle, C.c_void_p(dev.data_ptr()), n, policy, C.byref(eo), valid_mask,
+                                 C.byref(b) if best else None, C.c_void_p(s)))
+    if not best:
+        return EvalResult(obj, peak, flags, float("nan"), -1, -1)
+    return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
+
+
+def assignment_oracle(problem: Problem):
+    """assignment_oracle (solver.cpp:44-75): the full D^T save-all sweep on the
+    GPU; returns (best objective, device vector, placements evaluated)."""
+    obj, n = C.c_double(), C.c_int64()
+    dev = np.zeros(problem.T, np.int32)
+    check(LIB.xe_assignment_oracle(problem.handle, C.byref(obj), dev.ctypes.data, C.byref(n)))
+    return obj.value, dev, n.value
+
+
 class _DevArray:
     """__cuda_array_interface__ view of a device pointer owned by the library."""
 

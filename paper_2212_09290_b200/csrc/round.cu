@@ -239,7 +239,61 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   }
 }
 
+// Uniform random placements (K2b input, config 5's sweep): op i on a device
+// drawn uniformly from those that can run it (cost below the 1e9 sentinel);
+// one Philox block per (candidate, 4 consecutive ops), so a placement is a
+// pure function of (seed, global index) like the cubes.
+__global__ void placement_kernel(const uint8_t* allowed, const uint8_t* n_allowed, int D, int T, uint64_t seed,
+                                 int64_t first, int64_t n, uint8_t* out) {
+  const int64_t quads = (T + 3) / 4;
+  const int64_t total = n * quads;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < total;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = k / quads;
+    const int q = static_cast<int>(k % quads);
+    Philox rng(seed, static_cast<uint64_t>(first + c), 0x20000u + static_cast<uint32_t>(q));
+    const uint4 r = rng.next();
+    const uint32_t rv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = 4 * q + j;
+      if (i >= T) break;
+      const int cnt = n_allowed[i];
+      const int pick = static_cast<int>((static_cast<uint64_t>(rv[j]) * cnt) >> 32);
+      out[c * T + i] = allowed[i * D + pick];
+    }
+  }
+}
+
 }  // namespace
+
+void random_placements_device(const xe_problem* pr, uint64_t seed, int64_t first, int64_t n, uint8_t* out,
+                              cudaStream_t s) {
+  const HostProblem& h = pr->h;
+  std::vector<uint8_t> allowed(static_cast<size_t>(h.T) * h.D, 0), cnt(static_cast<size_t>(h.T), 0);
+  for (int i = 0; i < h.T; ++i) {
+    int best = 0;
+    for (int d = 0; d < h.D; ++d) {
+      const double c = h.cost[static_cast<size_t>(d) * h.T + i];
+      if (c < h.cost[static_cast<size_t>(best) * h.T + i]) best = d;
+      if (c < 1.0e9) allowed[static_cast<size_t>(i) * h.D + cnt[static_cast<size_t>(i)]++] = static_cast<uint8_t>(d);
+    }
+    if (!cnt[static_cast<size_t>(i)]) {  // every device prohibitive: the cheapest
+      allowed[static_cast<size_t>(i) * h.D] = static_cast<uint8_t>(best);
+      cnt[static_cast<size_t>(i)] = 1;
+    }
+  }
+  DevBuf<uint8_t> d_allowed, d_cnt;
+  d_allowed.upload(allowed, s);
+  d_cnt.upload(cnt, s);
+  int nsm = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+  if (n > 0) {
+    placement_kernel<<<nsm * 16, 256, 0, s>>>(d_allowed.p, d_cnt.p, h.D, h.T, seed, first, n, out);
+    XE_CUDA(cudaGetLastError());
+  }
+  XE_CUDA(cudaStreamSynchronize(s));  // the tables above are freed on return
+}
 
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
                         int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s) {

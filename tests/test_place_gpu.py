@@ -97,3 +97,31 @@ def test_assignment_oracle_pins():
         assert o == pn[f"rand{seed}"]["oracle"]
         assert dev.tolist() == pn[f"rand{seed}"]["oracle_dev"]
         assert pn[f"rand{seed}"]["exact"] <= o + 1e-9  # oracle dominance (test_properties.cpp:71-75)
+
+
+@pytest.mark.parametrize("name", ["fig2", "random2000"])
+def test_random_placements_generator_and_api(oracle, name):
+    """K4-style placement generator (config 5's sweep input): index-deterministic,
+    never on a prohibitive device; the Python API agrees with the CPU oracle."""
+    text = golden_problem_text("fig2") if name == "fig2" else configs.random2000_doc()
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    n = 4000 if name == "fig2" else 48
+    dev = xe.random_placements(prob, n, seed=9)
+    parts = torch.cat([xe.random_placements(prob, n // 2, seed=9), xe.random_placements(prob, n - n // 2, seed=9, first=n // 2)])
+    assert torch.equal(dev, parts)
+    dv = dev.cpu().numpy()
+    cost = np.asarray(a.cost).reshape(a.D, a.T)
+    assert (cost[dv, np.arange(a.T)[None, :]] < 1e9).all()
+    assert len(np.unique(dv[:, 1:])) == a.D
+    for pol in (0, 1):
+        r = xe.evaluate_placements(prob, dev, policy=pol)
+        ro, rp, rf = oracle.eval_placements(a, dv, pol)
+        assert np.array_equal(r.obj.cpu().numpy().view(np.int64), ro.view(np.int64))
+        assert np.array_equal(r.peak.cpu().numpy(), rp)
+        assert np.array_equal(r.flags.cpu().numpy().view(np.uint32) & 0xFFFF, rf & 0xFFFF)
+
+
+def test_oracle_python_api_fig2():
+    obj, dev, n = xe.assignment_oracle(xe.Problem.from_json(golden_problem_text("fig2")))
+    assert obj == 11.0 and n == 128 and dev[1] == 0  # A on the cpu (test_solver.cpp:99-119)
