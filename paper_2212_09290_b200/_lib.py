@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libxengine_b200.so")
+# XE_LIB overrides the library path (A/B builds of the same sources)
+LIB_PATH = os.environ.get("XE_LIB", os.path.join(HERE, "lib", "libxengine_b200.so"))
 
 XE_OK = 0
 XE_ERR_NO_DEVICE = 103

@@ -43,6 +43,9 @@ using cube::row_peak_general;
 using cube::TState;
 
 constexpr int kWarps = 8;
+#ifndef XE_IL_INCR_BASE
+#define XE_IL_INCR_BASE 1  // saved-tensor mass carried across t (0: byte tables every row; A/B builds)
+#endif
 // fixed shared-memory prefix (T <= 64): byte tables [8][256], masses [64],
 // parent / consumer masks [64]
 constexpr int kOffMtab = 0, kOffMass = 8 * 256 * 8, kOffPmask = kOffMass + 64 * 8, kOffCons = kOffPmask + 64 * 8,
@@ -173,8 +176,8 @@ __device__ __forceinline__ uint32_t decode_freed(const uint64_t* R, const uint64
 // M: integer type of tensor masses and memory sums (int32 when twice the
 // save-all total fits, halving the table traffic; int64 otherwise).
 // NBYTES: bytes of a bit row summed through the byte tables (4 for T <= 32,
-// else 8; tables beyond the problem's bytes are zero), so every lookup is
-// unconditional.
+// 6 for T <= 48, else 8; tables beyond the problem's bytes are zero), so
+// every lookup is unconditional.
 template <int MAXD, class M, int NBYTES>
 __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 1)) eval_il_kernel(const IlArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -229,6 +232,18 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
   for (int i = lane; i < 32 * MAXD; i += 32) s_pk[i] = 0;
   __syncthreads();
   const double* copy_glob = P.table + n_dt;  // copy terms in global memory (large E*D*D)
+  auto mass_bytes = [&](uint64_t x) {  // mass of a bit row through the byte tables
+    M m = 0;
+    const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+#pragma unroll
+    for (int b = 0; b < NBYTES; ++b) m += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+    return m;
+  };
+  auto sparse_mass = [&](uint64_t x) {  // mass of a row with few bits: first bit without a branch
+    M m = x ? s_mass[__ffsll(x) - 1] : M(0);
+    for (x &= x - 1; x; x &= x - 1) m += s_mass[__ffsll(x) - 1];
+    return m;
+  };
   int q_cnt = 0;  // warp-uniform
   auto drain = [&]() {
     __syncwarp();
@@ -307,6 +322,9 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
         Sn[d] = d < D ? ldS(d, 0) : 0ull;
       }
       const bool by_dst = P.edges_by_dst != 0;
+      M base_d[MAXD];
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) base_d[d] = d < D ? mass_bytes(Sn[d]) : M(0);
       for (int t = 0; t < T; ++t) {
         const bool more = t + 1 < T;
         uint64_t rany = 0, zany = 0, sor = 0, bad = 0;
@@ -328,10 +346,11 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
 #pragma unroll
         for (int d = 0; d < MAXD; ++d) {
           if (d >= D) continue;
-          M base = 0;
-          const uint32_t lo = static_cast<uint32_t>(S[d]), hi = static_cast<uint32_t>(S[d] >> 32);
-#pragma unroll
-          for (int b = 0; b < NBYTES; ++b) base += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+#if XE_IL_INCR_BASE
+          const M base = base_d[d];  // mass of S(d,t)
+#else
+          const M base = mass_bytes(S[d]);
+#endif
           const uint64_t r = R[d];
           const bool multi = (r & (r - 1)) != 0;
           const unsigned ballot = __ballot_sync(0xffffffffu, multi);
@@ -348,6 +367,20 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
           pk[d] = max(pk[d], r ? base + s_mass[__ffsll(r) - 1] : base);  // <= the deferred peak when multi
         }
         if (q_cnt > a.q_cap - 32 * D) drain();
+        // mass of S(d,t+1): when EQ11 holds, S(d,t+1) only gains tensors
+        // computed at t, so base(t+1) = base(t) + mass(R & Sn \ S) - mass(S \ Sn)
+        // (a few bits); otherwise the byte tables
+        if (XE_IL_INCR_BASE && more) {
+#pragma unroll
+          for (int d = 0; d < MAXD; ++d) {
+            if (d >= D) continue;
+            if (bad) {
+              base_d[d] = mass_bytes(Sn[d]);
+            } else {
+              base_d[d] += sparse_mass(R[d] & Sn[d] & ~S[d]) - sparse_mass(S[d] & ~Sn[d]);
+            }
+          }
+        }
 
         // ---- the computations of timestep t: dependencies (EQ12), decode's
         // copy sources, and (edges sorted by dst) the copy charges in
@@ -534,7 +567,7 @@ int align16(int x) { return (x + 15) & ~15; }
 
 template <int MAXD, class M>
 int launch_m(const IlArgs& a, cudaStream_t s, int nsm) {
-  auto k = a.P.T <= 32 ? eval_il_kernel<MAXD, M, 4> : eval_il_kernel<MAXD, M, 8>;
+  auto k = a.P.T <= 32 ? eval_il_kernel<MAXD, M, 4> : a.P.T <= 48 ? eval_il_kernel<MAXD, M, 6> : eval_il_kernel<MAXD, M, 8>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes));
   int per_sm = 0;
   XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarps * 32, a.smem_bytes));

@@ -288,11 +288,11 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   a.T = h.T;
   a.E = h.E;
   a.policy = policy;
-  a.fix_k = pr->fix_k_plain;
+  a.fix_k = pr->fix_k_place;
   a.mass = pr->d_mass.p;
   a.cost = pr->d_cost.p;
   a.w = pr->d_w.p;
-  a.tfix = pr->d_tfix_noenergy.p;
+  a.tfix = pr->d_tfix_place.p;
   a.src = pr->d_src.p;
   a.dst = pr->d_dst.p;
   a.eorder = eorder.p;
@@ -315,7 +315,7 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   a.wvalid = reinterpret_cast<int64_t*>(scratch + nw_max * 16);
   const int tb = (h.T + 15) & ~15;
   const int smem = place::kWarps * (tb + 128);
-  const bool exact = pr->fix_k_plain >= 0;
+  const bool exact = pr->fix_k_place >= 0;
   auto k = exact ? place::place_kernel<true> : place::place_kernel<false>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;

@@ -22,9 +22,9 @@ namespace xe {
 // the same double, and the kernels may accumulate in int64 fixed point.
 // Returns -1 when no such k exists (the kernels then reproduce the
 // reference's summation order term by term).
-int exact_fix_k(const std::vector<double>& table, int T) {
+// Same rule with an explicit bound on the largest possible total.
+int exact_fix_k_bound(const std::vector<double>& table, long double bound) {
   int k = 0;
-  long double bound = 0.0L;
   for (double v : table) {
     if (!std::isfinite(v)) return -1;
     if (v == 0.0) continue;
@@ -34,12 +34,16 @@ int exact_fix_k(const std::vector<double>& table, int T) {
     int tz = __builtin_ctzll(M);
     int need = -(e - 53 + tz);                                 // fractional bits
     k = std::max(k, need);
-    bound += std::fabs(static_cast<long double>(v));
   }
   if (k > 60) return -1;
-  bound *= static_cast<long double>(T);
   if (std::ldexp(bound, k) >= std::ldexp(1.0L, 52)) return -1;
   return k;
+}
+
+int exact_fix_k(const std::vector<double>& table, int T) {
+  long double bound = 0.0L;
+  for (double v : table) bound += std::fabs(static_cast<long double>(v));
+  return exact_fix_k_bound(table, bound * static_cast<long double>(T));
 }
 
 DevProblem xe_problem_view_impl(const xe_problem* p, bool energy);
@@ -113,6 +117,20 @@ void upload_problem(xe_problem* pr) {
   {
     std::vector<double> plain(pr->table.begin(), pr->table.begin() + D * T + E * D * D);
     pr->fix_k_plain = exact_fix_k(plain, T);
+    // a placement computes each op once and charges each edge at most once
+    // (save_all_assignment, solver.cpp:30-42): a much smaller worst case
+    long double pb = 0.0L;
+    for (int i = 0; i < T; ++i) {
+      double mx = 0.0;
+      for (int d = 0; d < D; ++d) mx = std::max(mx, std::fabs(h.cost[static_cast<size_t>(d) * T + i]));
+      pb += mx;
+    }
+    for (int e = 0; e < E; ++e) {
+      double mx = 0.0;
+      for (int k2 = 0; k2 < D * D; ++k2) mx = std::max(mx, std::fabs(pr->table[static_cast<size_t>(D * T + e * D * D + k2)]));
+      pb += mx;
+    }
+    pr->fix_k_place = exact_fix_k_bound(plain, pb);
     pr->fix_k_energy = h.has_energy ? exact_fix_k(pr->table, T) : pr->fix_k_plain;
   }
   auto fixed = [&](int k, bool with_energy) {
@@ -156,6 +174,7 @@ void upload_problem(xe_problem* pr) {
   pr->d_w.upload(h.w.empty() ? std::vector<double>(1, 0.0) : h.w, s);
   pr->d_tfix.upload(fixed(pr->fix_k_energy, true), s);
   pr->d_tfix_noenergy.upload(fixed(pr->fix_k_plain, false), s);
+  pr->d_tfix_place.upload(fixed(pr->fix_k_place, false), s);
   XE_CUDA(cudaStreamSynchronize(s));
 
   DevProblem& v = pr->dev;

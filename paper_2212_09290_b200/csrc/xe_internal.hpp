@@ -156,9 +156,11 @@ struct xe_problem {
   xe::DevBuf<double> d_ubound, d_table, d_q, d_cost, d_w;
   xe::DevBuf<int64_t> d_tfix;
   xe::DevBuf<int64_t> d_tfix_noenergy;
+  xe::DevBuf<int64_t> d_tfix_place;
   // derived host tables
   std::vector<double> table;           // [n_table] with energy terms
   int fix_k_energy = -1, fix_k_plain = -1;
+  int fix_k_place = -1;  // exact mode for placement candidates (tighter bound)
   xe::DevProblem dev{};                // fields filled for the energy-free view
   xe::DevProblem view(bool energy) const;
   // scratch for batched evaluation
