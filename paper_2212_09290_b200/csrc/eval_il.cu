@@ -43,9 +43,6 @@ using cube::row_peak_general;
 using cube::TState;
 
 constexpr int kWarps = 8;
-#ifndef XE_IL_INCR_BASE
-#define XE_IL_INCR_BASE 1  // saved-tensor mass carried across t (0: byte tables every row; A/B builds)
-#endif
 // fixed shared-memory prefix (T <= 64): byte tables [8][256], masses [64],
 // parent / consumer masks [64]
 constexpr int kOffMtab = 0, kOffMass = 8 * 256 * 8, kOffPmask = kOffMass + 64 * 8, kOffCons = kOffPmask + 64 * 8,
@@ -122,8 +119,13 @@ __device__ __forceinline__ void smem_max(int64_t* p, int64_t v) {
 // EQ11 rows of timestep t (S(d,t+1,i) > S(d,t,i) + R(d,t,i)) and the EQ16_HI
 // rows that fail with them (eval_cube_kernel.cuh eq16_hi).
 template <int MAXD>
-__device__ __noinline__ uint32_t eq11_flags(const uint64_t* R, const uint64_t* S, const uint64_t* Sn, int D,
-                                            int strict, const uint64_t* s_cons) {
+struct Rows3 {  // rows of timestep t (R, S) and t+1 (Sn), passed by value to the rare paths
+  uint64_t R[MAXD], S[MAXD], Sn[MAXD];
+};
+
+template <int MAXD>
+__device__ __noinline__ uint32_t eq11_flags(const Rows3<MAXD> rows, int D, int strict, const uint64_t* s_cons) {
+  const uint64_t *R = rows.R, *S = rows.S, *Sn = rows.Sn;
   uint64_t allR = ~0ull;
   for (int d = 0; d < D; ++d) allR &= R[d];
   uint32_t fl = 0;
@@ -239,14 +241,10 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
     for (int b = 0; b < NBYTES; ++b) m += s_mtab[b * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
     return m;
   };
-  auto sparse_mass = [&](uint64_t x) {  // mass of a row with few bits: first bit without a branch
-    M m = x ? s_mass[__ffsll(x) - 1] : M(0);
-    for (x &= x - 1; x; x &= x - 1) m += s_mass[__ffsll(x) - 1];
-    return m;
-  };
   int q_cnt = 0;  // warp-uniform
   auto drain = [&]() {
     __syncwarp();
+#pragma unroll 1
     for (int k = lane; k < q_cnt; k += 32) {
       const PeakRow q = queue[k];
       const M rp = row_peak_nw1<M>(q.r, q.z, q.sn, q.scan, static_cast<M>(q.base), T, s_pmask, s_cons, s_mass);
@@ -322,9 +320,6 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
         Sn[d] = d < D ? ldS(d, 0) : 0ull;
       }
       const bool by_dst = P.edges_by_dst != 0;
-      M base_d[MAXD];
-#pragma unroll
-      for (int d = 0; d < MAXD; ++d) base_d[d] = d < D ? mass_bytes(Sn[d]) : M(0);
       for (int t = 0; t < T; ++t) {
         const bool more = t + 1 < T;
         uint64_t rany = 0, zany = 0, sor = 0, bad = 0;
@@ -340,17 +335,24 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
           bad |= Sn[d] & ~(R[d] | S[d]);
         }
         if (sor & (t >= 64 ? 0ull : (~0ull << t))) fl |= XE_F_FIXED_ZERO;
-        if (bad) fl |= eq11_flags<MAXD>(R, S, Sn, D, a.strict, s_cons);
+        if (bad) {
+          Rows3<MAXD> rows;
+#pragma unroll
+          for (int d = 0; d < MAXD; ++d) {
+            rows.R[d] = R[d];
+            rows.S[d] = S[d];
+            rows.Sn[d] = Sn[d];
+          }
+          fl |= eq11_flags<MAXD>(rows, D, a.strict, s_cons);
+        }
 
         // ---- U recurrence and per-device peaks (model.cpp:514-537)
 #pragma unroll
         for (int d = 0; d < MAXD; ++d) {
           if (d >= D) continue;
-#if XE_IL_INCR_BASE
-          const M base = base_d[d];  // mass of S(d,t)
-#else
+          // mass of S(d,t) through the byte tables (branch-free; carrying it
+          // across t with sparse bit loops measured 27% slower: divergence)
           const M base = mass_bytes(S[d]);
-#endif
           const uint64_t r = R[d];
           const bool multi = (r & (r - 1)) != 0;
           const unsigned ballot = __ballot_sync(0xffffffffu, multi);
@@ -367,21 +369,6 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
           pk[d] = max(pk[d], r ? base + s_mass[__ffsll(r) - 1] : base);  // <= the deferred peak when multi
         }
         if (q_cnt > a.q_cap - 32 * D) drain();
-        // mass of S(d,t+1): when EQ11 holds, S(d,t+1) only gains tensors
-        // computed at t, so base(t+1) = base(t) + mass(R & Sn \ S) - mass(S \ Sn)
-        // (a few bits); otherwise the byte tables
-        if (XE_IL_INCR_BASE && more) {
-#pragma unroll
-          for (int d = 0; d < MAXD; ++d) {
-            if (d >= D) continue;
-            if (bad) {
-              base_d[d] = mass_bytes(Sn[d]);
-            } else {
-              base_d[d] += sparse_mass(R[d] & Sn[d] & ~S[d]) - sparse_mass(S[d] & ~Sn[d]);
-            }
-          }
-        }
-
         // ---- the computations of timestep t: dependencies (EQ12), decode's
         // copy sources, and (edges sorted by dst) the copy charges in
         // objective_value's (e, dc, ds) order (model.cpp:399-411)
