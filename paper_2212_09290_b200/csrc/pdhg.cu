@@ -168,31 +168,84 @@ struct Iter {
 };
 
 // primal step: x+ = clip(x - tau (c - K'y)); xbar = 2x+ - x; running sum
-__global__ void primal_kernel(Iter it) {
+// dual step:   y+ = proj(y + sigma (b - K xbar)); running sum
+// Both half-steps run with G lanes per column / row (G a power of two
+// <= 32): each lane takes every G-th nonzero, a G-wide shuffle reduction
+// combines them, and lane 0 of the group applies the update.  Thread per row
+// walks ~5 nonzeros as a chain of dependent loads (offsets -> index ->
+// vector), which leaves the small relaxations latency-bound; G lanes cut the
+// chain to one nonzero each and coalesce the index/value loads.
+template <int G>
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, G);
+  return v;
+}
+
+template <int G>
+__global__ void primal_group_kernel(Iter it) {
   const double tau = it.step[0];
-  GRID_LOOP(j, it.n) {
-    double g = it.c[j];
-    for (int64_t q = it.cp[j]; q < it.cp[j + 1]; ++q) g -= it.cval[q] * it.y[it.row[q]];
-    const double x0 = it.x[j];
-    const double xn = fmin(fmax(x0 - tau * g, it.lb[j]), it.ub[j]);
-    it.xbar[j] = 2.0 * xn - x0;
-    it.x[j] = xn;
-    it.xsum[j] += xn;
+  const int gl = threadIdx.x & (G - 1);
+  const unsigned mask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / G;
+  for (int64_t j = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G; j < it.n; j += stride) {
+    double acc = 0.0;
+    for (int64_t q = it.cp[j] + gl; q < it.cp[j + 1]; q += G) acc += it.cval[q] * it.y[it.row[q]];
+    acc = group_sum<G>(acc, mask);
+    if (gl == 0) {
+      const double g = it.c[j] - acc;
+      const double x0 = it.x[j];
+      const double xn = fmin(fmax(x0 - tau * g, it.lb[j]), it.ub[j]);
+      it.xbar[j] = 2.0 * xn - x0;
+      it.x[j] = xn;
+      it.xsum[j] += xn;
+    }
   }
 }
 
-// dual step: y+ = proj(y + sigma (b - K xbar)); running sum
-__global__ void dual_kernel(Iter it) {
+template <int G>
+__global__ void dual_group_kernel(Iter it) {
   const double sigma = it.step[1];
-  GRID_LOOP(i, it.m) {
-    double s = 0.0;
-    for (int64_t k = it.rp[i]; k < it.rp[i + 1]; ++k) s += it.val[k] * it.xbar[it.col[k]];
-    double yn = it.y[i] + sigma * (it.b[i] - s);
-    const int8_t sn = it.sense[i];
-    if (sn == 'G') yn = fmax(yn, 0.0);
-    else if (sn == 'L') yn = fmin(yn, 0.0);
-    it.y[i] = yn;
-    it.ysum[i] += yn;
+  const int gl = threadIdx.x & (G - 1);
+  const unsigned mask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / G;
+  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G; i < it.m; i += stride) {
+    double acc = 0.0;
+    for (int64_t q = it.rp[i] + gl; q < it.rp[i + 1]; q += G) acc += it.val[q] * it.xbar[it.col[q]];
+    acc = group_sum<G>(acc, mask);
+    if (gl == 0) {
+      double yn = it.y[i] + sigma * (it.b[i] - acc);
+      const int8_t sn = it.sense[i];
+      if (sn == 'G') yn = fmax(yn, 0.0);
+      else if (sn == 'L') yn = fmin(yn, 0.0);
+      it.y[i] = yn;
+      it.ysum[i] += yn;
+    }
+  }
+}
+
+// group width for an average of `avg` nonzeros per vector
+inline int group_width(double avg) {
+  int g = 1;
+  while (g < 32 && g < avg) g <<= 1;
+  return std::max(2, g);
+}
+
+template <int G>
+void launch_half_steps(const Iter& it, int64_t m, int64_t n, cudaStream_t s, bool primal) {
+  const int64_t len = primal ? n : m;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((len * G + kB - 1) / kB, 148LL * 16)));
+  if (primal) primal_group_kernel<G><<<blocks, kB, 0, s>>>(it);
+  else dual_group_kernel<G><<<blocks, kB, 0, s>>>(it);
+}
+
+void launch_half_step(const Iter& it, int64_t m, int64_t n, int g, cudaStream_t s, bool primal) {
+  switch (g) {
+    case 2: return launch_half_steps<2>(it, m, n, s, primal);
+    case 4: return launch_half_steps<4>(it, m, n, s, primal);
+    case 8: return launch_half_steps<8>(it, m, n, s, primal);
+    case 16: return launch_half_steps<16>(it, m, n, s, primal);
+    default: return launch_half_steps<32>(it, m, n, s, primal);
   }
 }
 
@@ -432,13 +485,16 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   it.n = n;
 
   const int block = o.check_every > 0 ? o.check_every : 64;
+  // lanes per column (SpM'V) and per row (SpMV) from the average lengths
+  const int g_col = group_width(n ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0);
+  const int g_row = group_width(m ? static_cast<double>(nnz) / static_cast<double>(m) : 1.0);
   // captured graph of `block` iterations
   cudaGraph_t graph;
   cudaGraphExec_t gexec;
   XE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < block; ++k) {
-    primal_kernel<<<grid(n), kB, 0, s>>>(it);
-    dual_kernel<<<grid(m), kB, 0, s>>>(it);
+    launch_half_step(it, m, n, g_col, s, true);
+    launch_half_step(it, m, n, g_row, s, false);
   }
   XE_CUDA(cudaStreamEndCapture(s, &graph));
   XE_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
