@@ -116,12 +116,13 @@ __device__ __forceinline__ void smem_max(int64_t* p, int64_t v) {
   atomicMax(reinterpret_cast<long long*>(p), static_cast<long long>(v));
 }
 
-// EQ11 rows of timestep t (S(d,t+1,i) > S(d,t,i) + R(d,t,i)) and the EQ16_HI
-// rows that fail with them (eval_cube_kernel.cuh eq16_hi).
 template <int MAXD>
 struct Rows3 {  // rows of timestep t (R, S) and t+1 (Sn), passed by value to the rare paths
   uint64_t R[MAXD], S[MAXD], Sn[MAXD];
 };
+
+// EQ11 rows of timestep t (S(d,t+1,i) > S(d,t,i) + R(d,t,i)) and the EQ16_HI
+// rows that fail with them (eval_cube_kernel.cuh eq16_hi).
 
 template <int MAXD>
 __device__ __noinline__ uint32_t eq11_flags(const Rows3<MAXD> rows, int D, int strict, const uint64_t* s_cons) {
@@ -141,13 +142,16 @@ __device__ __noinline__ uint32_t eq11_flags(const Rows3<MAXD> rows, int D, int s
   return fl;
 }
 
+
 // decode(): a copy for a computation (dc, v <= t) comes from the lowest
 // device holding the parent u; illegal when that device freed u at an
 // earlier step of timestep t (schedule.cpp:52-71).
 template <int MAXD>
-__device__ __forceinline__ uint32_t decode_freed(const uint64_t* R, const uint64_t* S, const uint64_t* Sn,
-                                              const uint64_t* needD, uint64_t rany, int t, int D, int strict,
-                                              const uint64_t* s_cons) {
+__device__ __noinline__ uint32_t decode_freed(const Rows3<MAXD> rows, const Rows3<MAXD> need, uint64_t rany, int t,
+                                              int D, int strict, const uint64_t* s_cons) {
+  // by value: the caller's row arrays stay in registers (indexing them with a
+  // runtime device index here would move them to local memory every step)
+  const uint64_t *R = rows.R, *S = rows.S, *Sn = rows.Sn, *needD = need.R;
   uint64_t zany = 0;
   for (int d = 0; d < D; ++d) zany |= R[d] | S[d];
   const uint64_t le_t = t >= 63 ? ~0ull : ((2ull << t) - 1ull);
@@ -268,7 +272,8 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
     const bool live = c < a.n;
     const uint64_t* cw = a.il + static_cast<size_t>(g) * K * 32 + lane;
     auto ldR = [&](int d, int t) { return __ldg(cw + static_cast<size_t>(d * T + t) * 32) & valid; };
-    auto ldS = [&](int d, int t) { return __ldg(cw + static_cast<size_t>((D + d) * T + t) * 32) & valid; };
+    // device rows are T*32 words apart: offsets fixed per d, one base pointer per t
+    const int64_t TS = static_cast<int64_t>(T) * 32;
 
     uint32_t fl = 0;
     double total = 0.0;
@@ -314,21 +319,22 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
       // ================= pass A: t-major =================
       // rows of t in R[], S[]; rows of t+1 prefetched into Rn[], Sn[]
       uint64_t R[MAXD], S[MAXD], Rn[MAXD], Sn[MAXD];
+      const uint64_t* row = cw;  // word (R, d=0, t) of this lane's candidate
 #pragma unroll
       for (int d = 0; d < MAXD; ++d) {
-        Rn[d] = d < D ? ldR(d, 0) : 0ull;
-        Sn[d] = d < D ? ldS(d, 0) : 0ull;
+        Rn[d] = d < D ? __ldg(row + d * TS) & valid : 0ull;
+        Sn[d] = d < D ? __ldg(row + (D + d) * TS) & valid : 0ull;
       }
       const bool by_dst = P.edges_by_dst != 0;
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < T; ++t, row += 32) {
         const bool more = t + 1 < T;
         uint64_t rany = 0, zany = 0, sor = 0, bad = 0;
 #pragma unroll
         for (int d = 0; d < MAXD; ++d) {
           R[d] = Rn[d];
           S[d] = Sn[d];
-          Rn[d] = (d < D && more) ? ldR(d, t + 1) : 0ull;
-          Sn[d] = (d < D && more) ? ldS(d, t + 1) : 0ull;
+          Rn[d] = (d < D && more) ? __ldg(row + 32 + d * TS) & valid : 0ull;
+          Sn[d] = (d < D && more) ? __ldg(row + 32 + (D + d) * TS) & valid : 0ull;
           rany |= R[d];
           zany |= R[d] | S[d];
           sor |= S[d];
@@ -432,7 +438,18 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
 #pragma unroll
           for (int d = 0; d < MAXD; ++d)
             if (d < D) missing |= needD[d] & ~(R[d] | S[d]) & zany;
-          if (missing) fl |= decode_freed<MAXD>(R, S, Sn, needD, rany, t, D, a.strict, s_cons);
+          if (missing) {
+            Rows3<MAXD> rows, need;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) {
+              rows.R[d] = R[d];
+              rows.S[d] = S[d];
+              rows.Sn[d] = Sn[d];
+              need.R[d] = needD[d];
+              need.S[d] = need.Sn[d] = 0;
+            }
+            fl |= decode_freed<MAXD>(rows, need, rany, t, D, a.strict, s_cons);
+          }
         }
         if (copies_left) {  // edge order not monotone in dst: ordered walk
           TState<NW, MAXD> st;
