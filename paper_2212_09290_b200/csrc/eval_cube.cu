@@ -90,7 +90,9 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
   a.cube_words = static_cast<uint32_t>(2 * P.D * P.T * P.W32);
   const int cube_bytes = static_cast<int>(a.cube_words * 4);
   a.use_bulk = (cube_bytes % 16 == 0) && (reinterpret_cast<uintptr_t>(cubes) % 16 == 0);
-  a.stages = 2;
+  // double-buffer small cubes; a large cube (configs 3-4: 17-22 KB) single-buffered,
+  // so twice as many warps fit the shared memory plan
+  a.stages = cube_bytes > 8192 ? 1 : 2;
 
   // shared-memory plan
   int off = 0;
@@ -132,11 +134,14 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
     x = align16(x + kSlots * (8 + 4 + 4 + 4) + 8 * kSlots * P.D + 2 * 32 * kCopyScratch);
     return x;
   };
-  // prefer two resident CTAs per SM (occupancy), else the most warps that fit
-  int warps = kWarps;
+  // the most resident warps per SM: two CTAs (tables duplicated) or one
+  // bigger CTA, whichever holds more
   const int two = smem_sm / 2 - 1024;
-  while (warps > 4 && a.off_warp + warps * warp_total(cap, cap2) > two) --warps;
-  while (warps > 1 && a.off_warp + warps * warp_total(cap, cap2) > smem_limit) --warps;
+  int w2 = kWarps, w1 = kWarps;
+  while (w2 > 1 && a.off_warp + w2 * warp_total(cap, cap2) > two) --w2;
+  while (w1 > 1 && a.off_warp + w1 * warp_total(cap, cap2) > smem_limit) --w1;
+  if (a.off_warp + w2 * warp_total(cap, cap2) > two) w2 = 0;
+  int warps = 2 * w2 >= w1 ? w2 : w1;
   while (!exact && cap > 16 && a.off_warp + warps * warp_total(cap, cap2) > smem_limit) {
     cap /= 2;
     cap2 = cap2 ? cap : 0;

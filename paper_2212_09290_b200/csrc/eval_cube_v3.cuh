@@ -122,11 +122,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) eval_cube_v3(const EvalArgs a)
     const int nslot = static_cast<int>(a.n - first < kSlots ? a.n - first : kSlots);
     for (int s = 0; s < nslot; ++s, ++k) {
       const int stage = static_cast<int>(k % a.stages);
-      {
-        const int64_t nk = k + 1;
-        const int64_t nc = (nk % kSlots == 0) ? cand_of(nk) : (s + 1 < nslot ? first + s + 1 : a.n);
-        issue(nc, static_cast<int>(nk % a.stages));
-      }
+      const int64_t next_c = ((k + 1) % kSlots == 0) ? cand_of(k + 1) : (s + 1 < nslot ? first + s + 1 : a.n);
+      if (a.stages > 1) issue(next_c, static_cast<int>((k + 1) % a.stages));  // prefetch into the other buffer
       if (a.use_bulk) {
         mbar_wait(&bars[stage], (phase_bits >> stage) & 1u);
         phase_bits ^= 1u << stage;
@@ -243,6 +240,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) eval_cube_v3(const EvalArgs a)
           }
           if (andnot(need_all, st.Zany).any()) fl |= XE_F_EQ12;
           if (andnot(need_le, st.Zany).any()) fl |= XE_F_DECODE;
+          // a copy source can free its tensor within timestep t only if it
+          // computes something at t, and it never computes the consumer: an
+          // illegal copy needs >= 2 devices computing at t
+          int busy = 0;
+#pragma unroll
+          for (int x = 0; x < MAXD; ++x) busy += (x < D && st.R[x].any()) ? 1 : 0;
 #pragma unroll
           for (int dc = 0; dc < MAXD; ++dc) {
             if (dc >= D) continue;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) eval_cube_v3(const EvalArgs a)
               if (ds < D && ds != dc) others = others | st.Z[ds];
             if ((needAllD[dc] & others).any()) has_copy = true;
             // decode: copy source = lowest holder; illegal if it freed u earlier
-            Row<NW> miss = andnot(needD[dc], st.Z[dc]) & st.Zany;
+            Row<NW> miss = busy >= 2 ? andnot(needD[dc], st.Z[dc]) & st.Zany : Row<NW>::zero();
             for (int u = miss.lsb(); u >= 0; miss.clear(u), u = miss.lsb()) {
               int sdev = 0;
 #pragma unroll
@@ -349,6 +352,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) eval_cube_v3(const EvalArgs a)
         slot_cnt2[s] = a.energy ? sumR : 0;
       }
       __syncwarp();
+      if (a.stages == 1) issue(next_c, 0);  // single buffer: refill once this candidate is done
     }
 
     // ---- chain phase: lane s replays slot s's term list (serial mode)
