@@ -41,6 +41,7 @@ struct Args {
   const double* cost;     // [D][T]
   const double* w;        // [E][D][D]
   const int64_t* tfix;    // [D*T + E*D*D] fixed point
+  const int64_t* tfix_edge;  // [E] when every cross-device copy of an edge costs the same (else null)
   const int32_t* src;
   const int32_t* dst;
   const int32_t* eorder;  // edges sorted by (dst, e)
@@ -66,15 +67,28 @@ __global__ void __launch_bounds__(kWarps * 32) place_kernel(const Args a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int T = a.T, D = a.D, E = a.E;
   const int tb = (T + 15) & ~15;
-  uint8_t* sdev = smem + wid * (tb + 8 * 8 * 2);
+  // edge endpoints packed (src | dst << 16) in shared memory, then one
+  // placement buffer per warp
+  uint32_t* s_edge = reinterpret_cast<uint32_t*>(smem);
+  const int eb = (4 * E + 15) & ~15;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    s_edge[e] = static_cast<uint32_t>(a.src[e]) | (static_cast<uint32_t>(a.dst[e]) << 16);
+  uint8_t* sdev = smem + eb + wid * tb;
+  __syncthreads();
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
   const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
   uint64_t best_key = ~0ull;
   int64_t best_idx = -1, n_valid = 0;
+  const bool vec = (T % 16) == 0 && (reinterpret_cast<uintptr_t>(a.dev) % 16) == 0;
 
   for (int64_t c = gw; c < a.n; c += nw) {
     const uint8_t* g = a.dev + c * T;
-    for (int i = lane; i < T; i += 32) sdev[i] = g[i];
+    if (vec) {  // 16-byte loads: one warp instruction moves 512 bytes
+      for (int i = lane; i < T / 16; i += 32)
+        reinterpret_cast<uint4*>(sdev)[i] = __ldg(reinterpret_cast<const uint4*>(g) + i);
+    } else {
+      for (int i = lane; i < T; i += 32) sdev[i] = g[i];
+    }
     __syncwarp();
     // ---- objective
     double obj = 0.0;
@@ -82,9 +96,19 @@ __global__ void __launch_bounds__(kWarps * 32) place_kernel(const Args a) {
       int64_t fix = 0;
       for (int i = lane; i < T; i += 32) fix += a.tfix[sdev[i] * T + i];
       const int base = D * T;
-      for (int e = lane; e < E; e += 32) {
-        const int du = sdev[a.src[e]], dv = sdev[a.dst[e]];
-        if (du != dv) fix += a.tfix[base + (e * D + du) * D + dv];
+      if (a.tfix_edge) {  // one cost per edge: an 8E-byte table that stays in L1
+#pragma unroll 4
+        for (int e = lane; e < E; e += 32) {
+          const uint32_t sd = s_edge[e];
+          if (sdev[sd & 0xffffu] != sdev[sd >> 16]) fix += __ldg(a.tfix_edge + e);
+        }
+      } else {
+#pragma unroll 4
+        for (int e = lane; e < E; e += 32) {
+          const uint32_t sd = s_edge[e];
+          const int du = sdev[sd & 0xffffu], dv = sdev[sd >> 16];
+          if (du != dv) fix += __ldg(a.tfix + base + (e * D + du) * D + dv);
+        }
       }
       fix = warp_sum_i64(fix);
       obj = ldexp(static_cast<double>(fix), -a.fix_k);
@@ -293,6 +317,27 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   a.cost = pr->d_cost.p;
   a.w = pr->d_w.p;
   a.tfix = pr->d_tfix_place.p;
+  // copy cost uniform over device pairs per edge (a single link model, the
+  // config-5 generator): the compact per-edge table
+  DevBuf<int64_t> tedge;
+  if (pr->fix_k_place >= 0 && h.D > 1) {
+    bool uniform = true;
+    std::vector<int64_t> te(static_cast<size_t>(h.E));
+    for (int e = 0; e < h.E && uniform; ++e) {
+      const double w0 = h.w[(static_cast<size_t>(e) * h.D + 0) * h.D + 1];
+      for (int x = 0; x < h.D && uniform; ++x)
+        for (int y = 0; y < h.D; ++y)
+          if (x != y && h.w[(static_cast<size_t>(e) * h.D + x) * h.D + y] != w0) {
+            uniform = false;
+            break;
+          }
+      te[static_cast<size_t>(e)] = static_cast<int64_t>(std::ldexp(w0, pr->fix_k_place));
+    }
+    if (uniform && h.E > 0) {
+      tedge.upload(te, s);
+      a.tfix_edge = tedge.p;
+    }
+  }
   a.src = pr->d_src.p;
   a.dst = pr->d_dst.p;
   a.eorder = eorder.p;
@@ -314,7 +359,8 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   a.wbest_idx = reinterpret_cast<int64_t*>(scratch + nw_max * 8);
   a.wvalid = reinterpret_cast<int64_t*>(scratch + nw_max * 16);
   const int tb = (h.T + 15) & ~15;
-  const int smem = place::kWarps * (tb + 128);
+  if (h.T > 65535) fail(XE_ERR_TOO_LARGE, "placement evaluation supports T <= 65535");
+  const int smem = ((4 * h.E + 15) & ~15) + place::kWarps * tb;
   const bool exact = pr->fix_k_place >= 0;
   auto k = exact ? place::place_kernel<true> : place::place_kernel<false>;
   XE_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
