@@ -304,6 +304,12 @@ int xe_pdhg_solve(xe_csr* m, const xe_pdhg_opts* opts, xe_pdhg_result* res,
 int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int64_t first,
                    int64_t n, int32_t edits, double perturb, uint32_t* cubes_dev,
                    void* stream);
+/* Local-search neighbours of one canonical device cube (the incumbent):
+ * each is the base with (probability 1/2) one op moved, with its saves, to
+ * another device, then up to `edits` drop-and-recompute edits and an
+ * optional random bit flip; candidate k a pure function of (seed, first + k). */
+int xe_mutate_cubes(const xe_problem* p, const uint32_t* base_dev, uint64_t seed, int64_t first, int64_t n,
+                    int32_t edits, double perturb, uint32_t* cubes_dev, void* stream);
 /* n uniform random placements dev[n][T] (device buffer): op i on a device
  * that can run it (cost < 1e9), candidate k a pure function of
  * (seed, first + k) — the input family of config 5's placement sweep. */

@@ -218,6 +218,19 @@ def evaluate_cubes_il(problem: Problem, il, n: int, opts: Optional[ModelOptions]
     return EvalResult(obj, peak, flags, b.obj, b.index, b.n_valid)
 
 
+def mutate_cubes(problem: Problem, base, n: int, seed: int, first: int = 0, edits: int = 2,
+                 perturb: float = 0.0, out=None, stream=None):
+    """K4 local search: n neighbours of the canonical device cube `base`
+    (int32 CUDA tensor [cube_words])."""
+    import torch
+    if out is None:
+        out = torch.empty((n, problem.cube_words), dtype=torch.int32, device=base.device)
+    s = stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.xe_mutate_cubes(problem.handle, C.c_void_p(base.data_ptr()), seed, first, n, edits, perturb,
+                              C.c_void_p(out.data_ptr()), C.c_void_p(s)))
+    return out
+
+
 def random_placements(problem: Problem, n: int, seed: int, first: int = 0, out=None, stream=None):
     """n uniform random placements (uint8 CUDA tensor [n, T]); candidate k is
     a pure function of (seed, first + k)."""

@@ -24,7 +24,8 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
                        int64_t n, double* obj, int64_t* peak, uint32_t* flags, uint32_t valid_mask,
                        uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
-                        int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s);
+                        int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s,
+                        const uint32_t* base = nullptr);
 void random_placements_device(const xe_problem* pr, uint64_t seed, int64_t first, int64_t n, uint8_t* out,
                               cudaStream_t s);
 void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n, int policy, double* obj,
@@ -404,6 +405,16 @@ int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int6
     require_uploaded(p);
     cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     round_cubes_device(p, x_dev, seed, first, n, edits, perturb, cubes_dev, s);
+  });
+}
+
+int xe_mutate_cubes(const xe_problem* p, const uint32_t* base_dev, uint64_t seed, int64_t first, int64_t n,
+                    int32_t edits, double perturb, uint32_t* cubes_dev, void* stream) {
+  return guard([&] {
+    if (!p || !base_dev || (!cubes_dev && n > 0) || n < 0 || edits < 0) fail(XE_ERR_ARG, "bad argument");
+    require_uploaded(p);
+    round_cubes_device(p, nullptr, seed, first, n, edits, perturb, cubes_dev, static_cast<cudaStream_t>(stream),
+                       base_dev);
   });
 }
 

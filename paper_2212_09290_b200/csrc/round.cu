@@ -69,6 +69,7 @@ struct RoundArgs {
   const int32_t* in_ptr;
   const int32_t* in_edge;
   const double* x;      // LP solution or null
+  const uint32_t* base; // local search: every candidate starts from this cube (or null)
   int D, T, E, W32;
   int64_t r_base;       // column offset of R in x (0)
   uint64_t seed;
@@ -101,13 +102,43 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * kRoundWarps + wid; k < a.n;
        k += static_cast<int64_t>(gridDim.x) * kRoundWarps) {
     const uint64_t c = static_cast<uint64_t>(a.first + k);
-    for (int i = lane; i < words; i += 32) cube[i] = 0;
+    for (int i = lane; i < words; i += 32) cube[i] = a.base ? a.base[i] : 0u;
     // last consumer of every op (edge order independent)
     for (int i = lane; i < T; i += 32) last[i] = -1;
     __syncwarp();
     for (int e = lane; e < a.E; e += 32) atomicMax(&last[a.src[e]], a.dst[e]);
+    if (a.base) {
+      // local search around a base schedule: devices from its diagonal, then
+      // (probability 1/2) one op moved with its saves to another device, then
+      // the drop-and-recompute edits below
+      for (int i = lane; i < T; i += 32) {
+        int d0 = 0;
+        for (int d = D - 1; d >= 0; --d)
+          if (bit_get(0, d, i, i)) d0 = d;
+        dev[i] = d0;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        Philox rng(a.seed, c, 0x2u);
+        if (D > 1 && T > 1 && rng.uniform() < 0.5) {
+          const int i = 1 + rng.below(T - 1), from = dev[i];
+          const int to = (from + 1 + rng.below(D - 1)) % D;
+          if (a.cost[to * T + i] < 1.0e9) {
+            bit_clr(0, from, i, i);
+            bit_set(0, to, i, i);
+            for (int t = i + 1; t < T; ++t)
+              if (bit_get(1, from, t, i)) {
+                bit_clr(1, from, t, i);
+                bit_set(1, to, t, i);
+              }
+            dev[i] = to;
+          }
+        }
+      }
+      __syncwarp();
+    }
     // 1. placement, one Philox stream per (candidate, op)
-    for (int i = lane; i < T; i += 32) {
+    for (int i = lane; i < T && !a.base; i += 32) {
       Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
       double tot = 0.0;
       for (int d = 0; d < D; ++d) {
@@ -135,7 +166,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
     }
     __syncwarp();
     // 2. diagonal + minimal-save
-    for (int i = lane; i < T; i += 32) {
+    for (int i = lane; i < T && !a.base; i += 32) {
       bit_set(0, dev[i], i, i);
       for (int t = i + 1; t <= last[i]; ++t) bit_set(1, dev[i], t, i);
     }
@@ -296,9 +327,11 @@ void random_placements_device(const xe_problem* pr, uint64_t seed, int64_t first
 }
 
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
-                        int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s) {
+                        int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s,
+                        const uint32_t* base) {
   const HostProblem& h = pr->h;
   RoundArgs a{};
+  a.base = base;
   a.mass = pr->d_mass.p;
   a.cost = pr->d_cost.p;
   a.src = pr->d_src.p;

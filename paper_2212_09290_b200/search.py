@@ -24,7 +24,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .api import ModelOptions, Problem, build_model, evaluate_cubes, pdhg_solve, round_cubes
+from .api import ModelOptions, Problem, build_model, evaluate_cubes, mutate_cubes, pdhg_solve, round_cubes
 
 # a schedule is usable when check_assignment passes, every device stays
 # within its integer budget (solver.cpp:237,249) and it decodes (schedule.cpp:40-129)
@@ -41,12 +41,14 @@ class SearchResult:
     lp_certified: bool
     n_evaluated: int
     n_valid: int
+    ls_improvements: int = 0    # incumbent improvements found by the local search
 
 
 def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: int = 1 << 18,
            rounds: int = 4, seed: int = 1, edits: int = 3, use_lp: bool = True,
            valid_mask: int = DEFAULT_MASK, first: int = 0, lp_tol: float = 1e-6,
-           distributed: bool = False) -> SearchResult:
+           distributed: bool = False, ls_rounds: int = 0, ls_n: int = 1 << 16,
+           ls_edits: int = 2) -> SearchResult:
     """distributed=True (torch.distributed initialised, one process per GPU):
     rank r evaluates global index blocks (round * world + r) * n_per_round,
     the incumbent is exchanged with shard.exchange_best; every rank returns
@@ -77,10 +79,25 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
         inc = exchange_best(best_obj, best_idx, n_valid, offset=0, device="cuda")
         best_obj, best_idx, n_valid = inc.obj, inc.index, inc.n_valid
     cube = peaks = None
+    n_eval = rounds * n_per_round * world
+    improvements = 0
     if best_idx >= 0:
         c = round_cubes(problem, 1, seed, first=best_idx, edits=edits, perturb=0.0, x=x_dev)
         r1 = evaluate_cubes(problem, c, opts, valid_mask=valid_mask)
         assert r1.best_obj == best_obj, (r1.best_obj, best_obj)
-        cube = c.cpu().numpy().view(np.uint32)[0]
+        # K4 local search: hill-climb over neighbours of the incumbent (one
+        # op moved with its saves, drop-and-recompute edits), K2 scoring
+        inc = c[0].clone()
+        for it in range(ls_rounds):
+            nb = mutate_cubes(problem, inc, ls_n, seed ^ 0x5EED, first=it * ls_n, edits=ls_edits)
+            r2 = evaluate_cubes(problem, nb, opts, valid_mask=valid_mask, outputs=False)
+            n_eval += ls_n
+            if r2.best_index >= 0 and r2.best_obj < best_obj:
+                best_obj, inc = r2.best_obj, nb[r2.best_index].clone()
+                improvements += 1
+            del nb
+        r1 = evaluate_cubes(problem, inc.unsqueeze(0), opts, valid_mask=valid_mask)
+        assert r1.best_obj == best_obj, (r1.best_obj, best_obj)
+        cube = inc.cpu().numpy().view(np.uint32)
         peaks = r1.peak.cpu().numpy()[0]
-    return SearchResult(best_obj, best_idx, cube, peaks, lp_val, cert, rounds * n_per_round * world, n_valid)
+    return SearchResult(best_obj, best_idx, cube, peaks, lp_val, cert, n_eval, n_valid, improvements)
