@@ -70,6 +70,11 @@ struct RoundArgs {
   const int32_t* in_edge;
   const double* x;      // LP solution or null
   const uint32_t* base; // local search: every candidate starts from this cube (or null)
+  // LP-guided recomputation: off-diagonal R(d,t,i) (t > i) of the relaxation
+  // with weight > 0, as codes (d*T + t)*T + i and their cumulative weights
+  const int32_t* rc_code;
+  const double* rc_cdf;
+  int n_rc;
   int D, T, E, W32;
   int64_t r_base;       // column offset of R in x (0)
   uint64_t seed;
@@ -176,19 +181,35 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       Philox rng(a.seed, c, 0x1u);
       for (int ed = 0; ed < a.edits; ++ed) {
         if (rng.uniform() >= 0.6) continue;
-        // op i with a consumer beyond i+1, chosen uniformly among eligible ops
-        int n_el = 0;
-        for (int i = 0; i < T; ++i) n_el += last[i] > i + 1;
-        if (n_el == 0) break;
-        int pickn = rng.below(n_el), i = 0;
-        for (i = 0; i < T; ++i)
-          if (last[i] > i + 1 && pickn-- == 0) break;
-        // consumer t > i+1 of i, uniformly among its consumers
-        int n_c = 0;
-        for (int e = 0; e < a.E; ++e) n_c += (a.src[e] == i && a.dst[e] > i + 1);
-        int pc = rng.below(n_c), t = -1;
-        for (int e = 0; e < a.E; ++e)
-          if (a.src[e] == i && a.dst[e] > i + 1 && pc-- == 0) t = a.dst[e];
+        int i = 0, t = -1, lp_dev = -1;
+        if (a.n_rc > 0 && rng.uniform() < 0.7) {
+          // where the LP relaxation recomputes: (d, t, i) drawn with weight x(R(d,t,i))
+          const double u = rng.uniform() * a.rc_cdf[a.n_rc - 1];
+          int lo = 0, hi = a.n_rc - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (a.rc_cdf[mid] > u) hi = mid;
+            else lo = mid + 1;
+          }
+          const int code = a.rc_code[lo];
+          i = code % T;
+          t = code / T % T;
+          lp_dev = code / (T * T);
+        } else {
+          // op i with a consumer beyond i+1, chosen uniformly among eligible ops
+          int n_el = 0;
+          for (int j = 0; j < T; ++j) n_el += last[j] > j + 1;
+          if (n_el == 0) break;
+          int pickn = rng.below(n_el);
+          for (i = 0; i < T; ++i)
+            if (last[i] > i + 1 && pickn-- == 0) break;
+          // consumer t > i+1 of i, uniformly among its consumers
+          int n_c = 0;
+          for (int e = 0; e < a.E; ++e) n_c += (a.src[e] == i && a.dst[e] > i + 1);
+          int pc = rng.below(n_c);
+          for (int e = 0; e < a.E; ++e)
+            if (a.src[e] == i && a.dst[e] > i + 1 && pc-- == 0) t = a.dst[e];
+        }
         // the drop window must not cover a timestep where i is needed: any
         // earlier computation (diagonal or recomputed) of a consumer of i
         int a0 = i + 1;
@@ -203,8 +224,9 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
             }
           }
         if (a0 > t) continue;
-        const int a1 = a0 + rng.below(t - a0 + 1);
-        int dn = rng.uniform() < 0.5 ? rng.below(D) : dev[t];
+        // drop the whole window when the LP chose the spot, else a random tail of it
+        const int a1 = lp_dev >= 0 ? a0 : a0 + rng.below(t - a0 + 1);
+        int dn = lp_dev >= 0 ? lp_dev : (rng.uniform() < 0.5 ? rng.below(D) : dev[t]);
         if (a.cost[dn * T + i] >= 1.0e9) dn = dev[i];
         // recompute op v at t on dn, dropping its saves on dev-of-v over
         // [from, t]; later saves follow it to dn (EQ11 needs a holder at t)
@@ -339,6 +361,34 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.in_ptr = pr->d_in_ptr.p;
   a.in_edge = pr->d_in_edge.p;
   a.x = x;
+  DevBuf<int32_t> rc_code;
+  DevBuf<double> rc_cdf;
+  if (x) {  // LP off-diagonal R (columns (d*T + t)*T + i, t > i) with weight > 1e-6
+    const size_t nr = static_cast<size_t>(h.D) * h.T * h.T;
+    std::vector<double> xr(nr);
+    XE_CUDA(cudaMemcpyAsync(xr.data(), x, nr * 8, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> code;
+    std::vector<double> cdf;
+    double acc = 0.0;
+    for (int d = 0; d < h.D; ++d)
+      for (int t = 1; t < h.T; ++t)
+        for (int i = 0; i < t; ++i) {
+          const double v = xr[(static_cast<size_t>(d) * h.T + t) * h.T + i];
+          if (v > 1e-6 && h.cost[static_cast<size_t>(d) * h.T + i] < 1.0e9) {
+            acc += v;
+            code.push_back((d * h.T + t) * h.T + i);
+            cdf.push_back(acc);
+          }
+        }
+    if (!code.empty()) {
+      rc_code.upload(code, s);
+      rc_cdf.upload(cdf, s);
+      a.rc_code = rc_code.p;
+      a.rc_cdf = rc_cdf.p;
+      a.n_rc = static_cast<int>(code.size());
+    }
+  }
   a.D = h.D;
   a.T = h.T;
   a.E = h.E;
@@ -363,6 +413,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     round_kernel<<<grid, kRoundWarps * 32, smem, s>>>(a);
     XE_CUDA(cudaGetLastError());
   }
+  if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));  // the recompute list above is call-local
 }
 
 }  // namespace xe
