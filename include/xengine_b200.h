@@ -14,7 +14,11 @@
  *     + 1 (proj/include/xengine/errors.hpp:9-42), or XE_ERR_CUDA / XE_ERR_NCCL /
  *     XE_ERR_ARG.  xe_last_error() returns the thread-local message.
  *   - No exceptions cross this boundary; plain pointers and sizes only.
- *   - Handles are immutable after construction and bound to one CUDA stream.
+ *   - A handle's problem/model data never changes after construction, but
+ *     the handle also owns evaluation scratch (best-of-batch partials, the
+ *     staging buffers of the canonical/host entry points) and one CUDA
+ *     stream: use a handle from one host thread at a time (one handle per
+ *     thread or per GPU for concurrency).
  *   - Buffers documented "device" must be device pointers (cudaMalloc / torch
  *     CUDA tensors); "host" buffers may be pageable or pinned.
  */

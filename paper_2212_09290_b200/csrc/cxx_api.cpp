@@ -139,7 +139,9 @@ int default_device() {
 }
 
 // Resolved SoA image; the key is its byte content (a one-entry cache avoids
-// re-uploading the same problem for every objective_value call).
+// re-uploading the same problem for every objective_value call).  The cached
+// handle's scratch is shared, so the C++ API, like the reference's free
+// functions on one Problem, is meant for one host thread at a time.
 struct Desc {
   int D = 0, T = 0, E = 0;
   std::vector<int64_t> mass, budget;
