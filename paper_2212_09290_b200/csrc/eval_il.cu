@@ -390,9 +390,6 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
             if (x < D && x != d) elsewhere[d] |= R[x] | S[x];
         }
         bool copies_left = false;
-        // computations of t in ascending op order (the copy-charge order):
-        // recomputes below t, the diagonal op t (the same v for every lane),
-        // then any (fixed-zero violating) ops above t
         auto visit = [&](int v) {
           const uint64_t pm = s_pmask[v];
           need_all |= pm;
@@ -424,10 +421,9 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
             }
           }
         };
-        const uint64_t below_t = (1ull << t) - 1ull;
-        for (uint64_t rem = rany & below_t; rem; rem &= rem - 1) visit(__ffsll(rem) - 1);
-        if ((rany >> t) & 1ull) visit(t);
-        for (uint64_t rem = rany & ~below_t & ~(1ull << t); rem; rem &= rem - 1) visit(__ffsll(rem) - 1);
+        // ascending op order is the copy-charge order; one call site keeps
+        // the hot loop small (splitting off the diagonal op t measured equal)
+        for (uint64_t rem = rany; rem; rem &= rem - 1) visit(__ffsll(rem) - 1);
         if (need_all & ~zany) fl |= XE_F_EQ12;
         if (need_le & ~zany) fl |= XE_F_DECODE;
         // a copy source can free its tensor within timestep t only if it
