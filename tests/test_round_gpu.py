@@ -50,3 +50,25 @@ def test_perturbation_rate():
     f = r.flags.cpu().numpy().view(np.uint32)
     bad = ((f & STRUCTURAL) != 0).mean()
     assert 0.02 < bad < 0.12  # single flips break a structural family most of the time
+
+
+def test_local_search_neighbours(oracle):
+    """xe_mutate_cubes: neighbours of an incumbent are index-deterministic,
+    differ from it, keep the fixed-zero triangles, and the oracle agrees with
+    the GPU evaluation of every neighbour."""
+    text = configs.vgg16_doc()
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    base = xe.round_cubes(prob, 1, seed=4)[0]
+    nb = xe.mutate_cubes(prob, base, 512, seed=9, edits=2)
+    again = torch.cat([xe.mutate_cubes(prob, base, 200, seed=9, edits=2),
+                       xe.mutate_cubes(prob, base, 312, seed=9, first=200, edits=2)])
+    assert torch.equal(nb, again)
+    changed = (nb != base.unsqueeze(0)).any(dim=1).float().mean().item()
+    assert changed > 0.5
+    cubes = nb.cpu().numpy().view(np.uint32)
+    o, p, f = oracle.eval_cubes(a, cubes)
+    assert ((f & _lib.F_FIXED_ZERO) == 0).all()
+    r = xe.evaluate_cubes(prob, nb)
+    assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
+    assert np.array_equal(r.peak.cpu().numpy(), p)
