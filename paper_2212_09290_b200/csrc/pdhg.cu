@@ -12,8 +12,9 @@
 //
 // Saddle point  c'x - y'(Kx - b)  with y >= 0 on G rows, y <= 0 on L rows.
 // Iteration (tau = eta/omega, sigma = eta*omega):
-//   x+ = clip(x - tau (c - K'y), lb, ub)           one thread per column, CSC
-//   y+ = proj(y + sigma (b - K (2x+ - x)))          one thread per row, CSR
+//   x+ = clip(x - tau (c - K'y), lb, ub)           one lane per column
+//   y+ = proj(y + sigma (b - K (2x+ - x)))          one lane per row
+// over sliced, length-sorted copies of K and K' (see "sliced layout").
 // Preconditioning: rows normalised to unit inf-norm, then 10 Ruiz passes
 // (inf-norm) + Pock-Chambolle (alpha = 1); columns with the prohibitive cost
 // (>= 1e9) fixed at 0 and certified afterwards by their reduced costs; step
@@ -29,6 +30,9 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "csr.hpp"
 
 namespace xe {
@@ -42,11 +46,6 @@ inline int grid(int64_t n) {
 
 #define GRID_LOOP(i, n) \
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < (n); i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-
-__global__ void col_of_kernel(const int64_t* col_ptr, int64_t n, int32_t* col_of) {
-  GRID_LOOP(j, n)
-  for (int64_t q = col_ptr[j]; q < col_ptr[j + 1]; ++q) col_of[q] = static_cast<int32_t>(j);
-}
 
 // norm of each row of Dr*K*Dc: inf-norm (p=0) or l1 (p=1)
 __global__ void row_norm_kernel(const int64_t* rp, const int32_t* col, const double* val, const double* Dr,
@@ -137,29 +136,217 @@ __global__ void scale_b_kernel(const double* b, const double* Dr, int64_t m, dou
   GRID_LOOP(i, m) bs[i] = b[i] * Dr[i];
 }
 
-// y = K x  (CSR, thread per row)
-__global__ void spmv_kernel(const int64_t* rp, const int32_t* col, const double* val, const double* x, int64_t m,
-                            double* y) {
-  GRID_LOOP(i, m) {
-    double s = 0.0;
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += val[k] * x[col[k]];
-    y[i] = s;
+// ---- sliced layout (SELL-32 over length-sorted windows) -------------------
+// The half-steps run one lane per row (per column for K'y) over a sliced
+// copy of the scaled matrix.  Rows (columns) are reordered once: rows longer
+// than kLong first (longest first), then the rest sorted by descending
+// length inside windows of kSigma consecutive rows, so neighbouring rows stay
+// neighbours (locality of the gathered vector entries).  The short rows are
+// cut into slices of 32 stored column-major (entry t of lane l at
+// sptr[s] + 32 t + l) and padded to the slice's longest row (~1 % padding on
+// the configs-2/3 models); the long rows are stored row-major and taken by a
+// whole warp (lanes stride the entries, shuffle reduction), so no lane walks
+// a long row serially (the longest row of ResNet-50 cfg 3 has 435 entries).
+// The solve runs in the reordered index space — vectors permuted once,
+// indices remapped — so every per-row vector access and matrix load is a
+// coalesced 32-lane transaction, and a lane's chain of dependent loads is
+// (slice offset) -> (index, value) -> (gathered entry), with the per-row
+// operands issued before the dot product.  The grouped CSR kernels this
+// replaces (G lanes per row, shuffle reduction) were latency-bound at
+// 1.7 TB/s on ResNet-50 cfg 3 (profiles/r01_k3_resnet_full.txt).
+constexpr int kLong = 12;
+constexpr int kSigma = 1024;
+
+struct Sell {
+  DevBuf<int64_t> sptr;  // [0, nlong]: long-row offsets; then ns + 1 slice offsets
+  DevBuf<int32_t> idx;   // remapped (reordered-space) indices of the other dimension
+  DevBuf<double> v;
+  DevBuf<int32_t> perm;  // reordered position -> original row / column
+  DevBuf<int32_t> inv;   // original -> reordered position
+  DevBuf<int32_t> slen;  // lengths in reordered order
+  int64_t len = 0, nlong = 0, ns = 0;
+};
+
+struct SellView {
+  const int64_t* __restrict__ ptr;  // long offsets at [0, nlong], slice offsets at [nlong + 1 + s]
+  const int32_t* __restrict__ idx;
+  const double* __restrict__ v;
+  int64_t len, nlong, ns;
+};
+
+__global__ void sort_key_kernel(const int64_t* p, int64_t n, uint32_t* key, int32_t* iota,
+                                unsigned long long* nlong) {
+  GRID_LOOP(i, n) {
+    const int64_t len = p[i + 1] - p[i];
+    const uint32_t inv_len = 255u - static_cast<uint32_t>(len < 255 ? len : 255);
+    const bool lg = len > kLong;
+    key[i] = lg ? inv_len : ((static_cast<uint32_t>(1 + i / kSigma) << 8) | inv_len);
+    iota[i] = static_cast<int32_t>(i);
+    if (lg) atomicAdd(nlong, 1ull);
   }
 }
-// x = K' y  (CSC, thread per column)
-__global__ void spmtv_kernel(const int64_t* cp, const int32_t* row, const double* val, const double* y, int64_t n,
-                             double* x) {
-  GRID_LOOP(j, n) {
-    double s = 0.0;
-    for (int64_t q = cp[j]; q < cp[j + 1]; ++q) s += val[q] * y[row[q]];
-    x[j] = s;
+__global__ void perm_len_kernel(const int64_t* p, const int32_t* perm, int64_t n, int32_t* slen, int32_t* inv) {
+  GRID_LOOP(k, n) {
+    const int32_t i = perm[k];
+    slen[k] = static_cast<int32_t>(p[i + 1] - p[i]);
+    inv[i] = static_cast<int32_t>(k);
+  }
+}
+// sizes: long rows [0, nlong), then slice widths x 32 (slice max length)
+__global__ void sell_size_kernel(const int32_t* slen, int64_t len, int64_t nlong, int64_t ns, int64_t* sz) {
+  GRID_LOOP(k, nlong + ns + 2) {
+    int64_t v = 0;
+    if (k < nlong) {
+      v = slen[k];
+    } else if (k > nlong && k <= nlong + ns) {
+      const int64_t r0 = nlong + (k - nlong - 1) * 32;
+      int32_t w = 0;
+      for (int64_t r = r0; r < r0 + 32 && r < len; ++r) w = max(w, slen[r]);
+      v = 32 * static_cast<int64_t>(w);
+    }
+    sz[k] = v;
+  }
+}
+__global__ void sell_fill_kernel(const int64_t* p, const int32_t* idx_in, const double* v_in, const int32_t* perm,
+                                 const int32_t* remap, int64_t len, int64_t nlong, int64_t ns, const int64_t* ptr,
+                                 int32_t* idx, double* v) {
+  GRID_LOOP(k, nlong + ns * 32) {
+    if (k < nlong) {
+      const int32_t i = perm[k];
+      const int64_t q0 = p[i], l = p[i + 1] - q0, o = ptr[k];
+      for (int64_t t = 0; t < l; ++t) {
+        idx[o + t] = remap[idx_in[q0 + t]];
+        v[o + t] = v_in[q0 + t];
+      }
+      continue;
+    }
+    const int64_t r = k - nlong, sl = r >> 5, row = k;
+    const int lane = static_cast<int>(r & 31);
+    const int64_t base = ptr[nlong + 1 + sl], w = (ptr[nlong + 2 + sl] - base) >> 5;
+    int64_t q0 = 0, l = 0;
+    if (row < len) {
+      const int32_t i = perm[row];
+      q0 = p[i];
+      l = p[i + 1] - q0;
+    }
+    for (int64_t t = 0; t < w; ++t) {
+      const bool in = t < l;
+      idx[base + t * 32 + lane] = in ? remap[idx_in[q0 + t]] : 0;
+      v[base + t * 32 + lane] = in ? v_in[q0 + t] : 0.0;
+    }
+  }
+}
+template <typename T>
+__global__ void gather_kernel(const T* in, const int32_t* perm, int64_t n, T* out) {
+  GRID_LOOP(k, n) out[k] = in[perm[k]];
+}
+// out[perm[k]] = in[k] * D[k]
+__global__ void unpermute_scale_kernel(const double* in, const double* D, const int32_t* perm, int64_t n,
+                                       double* out) {
+  GRID_LOOP(k, n) out[perm[k]] = in[k] * D[k];
+}
+
+// reorder one dimension of the pattern (p = CSR row or CSC column offsets)
+void sell_plan(const int64_t* p, int64_t n, Sell& S, cudaStream_t s) {
+  S.len = n;
+  const int64_t nn = std::max<int64_t>(1, n);
+  DevBuf<uint32_t> key, key_out;
+  DevBuf<int32_t> iota;
+  DevBuf<unsigned long long> cnt;
+  key.alloc(nn);
+  key_out.alloc(nn);
+  iota.alloc(nn);
+  cnt.alloc(1);
+  S.perm.alloc(nn);
+  S.inv.alloc(nn);
+  S.slen.alloc(nn);
+  XE_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
+  sort_key_kernel<<<grid(n), kB, 0, s>>>(p, n, key.p, iota.p, cnt.p);
+  size_t tmp_bytes = 0;
+  XE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key_out.p, iota.p, S.perm.p,
+                                          static_cast<int>(n), 0, 32, s));
+  DevBuf<unsigned char> tmp;
+  tmp.alloc(std::max<size_t>(1, tmp_bytes));
+  XE_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, key.p, key_out.p, iota.p, S.perm.p,
+                                          static_cast<int>(n), 0, 32, s));
+  perm_len_kernel<<<grid(n), kB, 0, s>>>(p, S.perm.p, n, S.slen.p, S.inv.p);
+  unsigned long long nl = 0;
+  XE_CUDA(cudaMemcpyAsync(&nl, cnt.p, 8, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaStreamSynchronize(s));
+  S.nlong = static_cast<int64_t>(nl);
+  S.ns = (n - S.nlong + 31) / 32;
+  const int64_t np = S.nlong + S.ns + 2;
+  S.sptr.alloc(np);
+  sell_size_kernel<<<grid(np), kB, 0, s>>>(S.slen.p, n, S.nlong, S.ns, S.sptr.p);
+  size_t scan_bytes = 0;
+  XE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, S.sptr.p, S.sptr.p, static_cast<int>(np), s));
+  tmp.reserve(std::max<size_t>(1, scan_bytes));
+  XE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, scan_bytes, S.sptr.p, S.sptr.p, static_cast<int>(np), s));
+  XE_CUDA(cudaStreamSynchronize(s));  // temporaries freed on return
+}
+
+// fill from CSR/CSC (p, idx, v), indices remapped by `remap`
+void sell_fill(const int64_t* p, const int32_t* idx, const double* v, const int32_t* remap, Sell& S, cudaStream_t s) {
+  int64_t total = 0;
+  XE_CUDA(cudaMemcpyAsync(&total, S.sptr.p + S.nlong + S.ns + 1, 8, cudaMemcpyDeviceToHost, s));
+  XE_CUDA(cudaStreamSynchronize(s));
+  S.idx.alloc(std::max<int64_t>(1, total));
+  S.v.alloc(std::max<int64_t>(1, total));
+  sell_fill_kernel<<<grid(S.nlong + S.ns * 32), kB, 0, s>>>(p, idx, v, S.perm.p, remap, S.len, S.nlong, S.ns,
+                                                            S.sptr.p, S.idx.p, S.v.p);
+  XE_CUDA(cudaGetLastError());
+}
+
+SellView view(const Sell& S) { return SellView{S.sptr.p, S.idx.p, S.v.p, S.len, S.nlong, S.ns}; }
+
+__device__ __forceinline__ double warp_sum(double a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+
+// dot product of long row w with x, complete on every lane
+__device__ __forceinline__ double long_dot(const SellView& A, int64_t w, const double* __restrict__ x, int lane) {
+  const int64_t b = A.ptr[w], e = A.ptr[w + 1];
+  double acc = 0.0;
+  for (int64_t q = b + lane; q < e; q += 32) acc += __ldg(A.v + q) * __ldg(x + __ldg(A.idx + q));
+  return warp_sum(acc);
+}
+
+// dot product of this lane's row of slice sl with x
+__device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const double* __restrict__ x, int lane) {
+  const int64_t base = A.ptr[A.nlong + 1 + sl];
+  const int w = static_cast<int>((A.ptr[A.nlong + 2 + sl] - base) >> 5);
+  const int32_t* ip = A.idx + base + lane;
+  const double* vp = A.v + base + lane;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int t = 0; t < w; ++t) acc += __ldg(vp + 32 * t) * __ldg(x + __ldg(ip + 32 * t));
+  return acc;
+}
+
+#define WARP_ITEMS(w, A)                                                                                 \
+  const int lane = threadIdx.x & 31;                                                                     \
+  const int64_t nw_ = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;                               \
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < (A).nlong + (A).ns; \
+       w += nw_)
+
+// out = A x (rows of A in reordered order)
+__global__ void sell_spmv_kernel(SellView A, const double* __restrict__ x, double* __restrict__ out) {
+  WARP_ITEMS(w, A) {
+    if (w < A.nlong) {
+      const double acc = long_dot(A, w, x, lane);
+      if (lane == 0) out[w] = acc;
+    } else {
+      const int64_t sl = w - A.nlong, k = A.nlong + sl * 32 + lane;
+      const double acc = slice_dot(A, sl, x, lane);
+      if (k < A.len) out[k] = acc;
+    }
   }
 }
 
 struct Iter {
-  const int64_t *rp, *cp;
-  const int32_t *col, *row;
-  const double *val, *cval;
+  SellView R, C;  // rows of K, rows of K' (reordered spaces)
   const double *c, *lb, *ub, *b;
   const int8_t* sense;
   double *x, *xbar, *xsum, *y, *ysum;
@@ -168,85 +355,83 @@ struct Iter {
 };
 
 // primal step: x+ = clip(x - tau (c - K'y)); xbar = 2x+ - x; running sum
-// dual step:   y+ = proj(y + sigma (b - K xbar)); running sum
-// Both half-steps run with G lanes per column / row (G a power of two
-// <= 32): each lane takes every G-th nonzero, a G-wide shuffle reduction
-// combines them, and lane 0 of the group applies the update.  Thread per row
-// walks ~5 nonzeros as a chain of dependent loads (offsets -> index ->
-// vector), which leaves the small relaxations latency-bound; G lanes cut the
-// chain to one nonzero each and coalesce the index/value loads.
-template <int G>
-__device__ __forceinline__ double group_sum(double v, unsigned mask) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, G);
-  return v;
+__device__ __forceinline__ void primal_update(const Iter& it, int64_t j, double acc, double tau) {
+  const double x0 = it.x[j];
+  const double xn = fmin(fmax(x0 - tau * (__ldg(it.c + j) - acc), __ldg(it.lb + j)), __ldg(it.ub + j));
+  it.xbar[j] = 2.0 * xn - x0;
+  it.x[j] = xn;
+  it.xsum[j] += xn;
+}
+// dual step: y+ = proj(y + sigma (b - K xbar)); running sum
+__device__ __forceinline__ double dual_proj(double yn, int8_t sn) {
+  if (sn == 'G') return fmax(yn, 0.0);
+  if (sn == 'L') return fmin(yn, 0.0);
+  return yn;
 }
 
-template <int G>
-__global__ void primal_group_kernel(Iter it) {
+__global__ void __launch_bounds__(kB) primal_sell_kernel(Iter it) {
   const double tau = it.step[0];
-  const int gl = threadIdx.x & (G - 1);
-  const unsigned mask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / G;
-  for (int64_t j = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G; j < it.n; j += stride) {
-    double acc = 0.0;
-    for (int64_t q = it.cp[j] + gl; q < it.cp[j + 1]; q += G) acc += it.cval[q] * it.y[it.row[q]];
-    acc = group_sum<G>(acc, mask);
-    if (gl == 0) {
-      const double g = it.c[j] - acc;
-      const double x0 = it.x[j];
-      const double xn = fmin(fmax(x0 - tau * g, it.lb[j]), it.ub[j]);
+  WARP_ITEMS(w, it.C) {
+    if (w < it.C.nlong) {
+      const double acc = long_dot(it.C, w, it.y, lane);
+      if (lane == 0) primal_update(it, w, acc, tau);
+      continue;
+    }
+    const int64_t sl = w - it.C.nlong, j = it.C.nlong + sl * 32 + lane;
+    const bool on = j < it.n;
+    // per-column operands first, so their loads overlap the dot product
+    double cj = 0.0, x0 = 0.0, lo = 0.0, hi = 0.0, xs = 0.0;
+    if (on) {
+      cj = __ldg(it.c + j);
+      lo = __ldg(it.lb + j);
+      hi = __ldg(it.ub + j);
+      x0 = it.x[j];
+      xs = it.xsum[j];
+    }
+    const double acc = slice_dot(it.C, sl, it.y, lane);
+    if (on) {
+      const double xn = fmin(fmax(x0 - tau * (cj - acc), lo), hi);
       it.xbar[j] = 2.0 * xn - x0;
       it.x[j] = xn;
-      it.xsum[j] += xn;
+      it.xsum[j] = xs + xn;
     }
   }
 }
 
-template <int G>
-__global__ void dual_group_kernel(Iter it) {
+__global__ void __launch_bounds__(kB) dual_sell_kernel(Iter it) {
   const double sigma = it.step[1];
-  const int gl = threadIdx.x & (G - 1);
-  const unsigned mask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << ((threadIdx.x & 31) & ~(G - 1));
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x / G;
-  for (int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / G; i < it.m; i += stride) {
-    double acc = 0.0;
-    for (int64_t q = it.rp[i] + gl; q < it.rp[i + 1]; q += G) acc += it.val[q] * it.xbar[it.col[q]];
-    acc = group_sum<G>(acc, mask);
-    if (gl == 0) {
-      double yn = it.y[i] + sigma * (it.b[i] - acc);
-      const int8_t sn = it.sense[i];
-      if (sn == 'G') yn = fmax(yn, 0.0);
-      else if (sn == 'L') yn = fmin(yn, 0.0);
+  WARP_ITEMS(w, it.R) {
+    if (w < it.R.nlong) {
+      const double acc = long_dot(it.R, w, it.xbar, lane);
+      if (lane == 0) {
+        const double yn = dual_proj(it.y[w] + sigma * (__ldg(it.b + w) - acc), __ldg(it.sense + w));
+        it.y[w] = yn;
+        it.ysum[w] += yn;
+      }
+      continue;
+    }
+    const int64_t sl = w - it.R.nlong, i = it.R.nlong + sl * 32 + lane;
+    const bool on = i < it.m;
+    double bi = 0.0, y0 = 0.0, ys = 0.0;
+    int8_t sn = 'E';
+    if (on) {
+      bi = __ldg(it.b + i);
+      sn = __ldg(it.sense + i);
+      y0 = it.y[i];
+      ys = it.ysum[i];
+    }
+    const double acc = slice_dot(it.R, sl, it.xbar, lane);
+    if (on) {
+      const double yn = dual_proj(y0 + sigma * (bi - acc), sn);
       it.y[i] = yn;
-      it.ysum[i] += yn;
+      it.ysum[i] = ys + yn;
     }
   }
 }
 
-// group width for an average of `avg` nonzeros per vector
-inline int group_width(double avg) {
-  int g = 1;
-  while (g < 32 && g < avg) g <<= 1;
-  return std::max(2, g);
-}
-
-template <int G>
-void launch_half_steps(const Iter& it, int64_t m, int64_t n, cudaStream_t s, bool primal) {
-  const int64_t len = primal ? n : m;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((len * G + kB - 1) / kB, 148LL * 16)));
-  if (primal) primal_group_kernel<G><<<blocks, kB, 0, s>>>(it);
-  else dual_group_kernel<G><<<blocks, kB, 0, s>>>(it);
-}
-
-void launch_half_step(const Iter& it, int64_t m, int64_t n, int g, cudaStream_t s, bool primal) {
-  switch (g) {
-    case 2: return launch_half_steps<2>(it, m, n, s, primal);
-    case 4: return launch_half_steps<4>(it, m, n, s, primal);
-    case 8: return launch_half_steps<8>(it, m, n, s, primal);
-    case 16: return launch_half_steps<16>(it, m, n, s, primal);
-    default: return launch_half_steps<32>(it, m, n, s, primal);
-  }
+inline int items_grid(const Sell& S) {
+  const int64_t items = S.nlong + S.ns;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((items + kB / 32 - 1) / (kB / 32), 148LL * 16)));
 }
 
 // partial sums for the KKT measures, 8 doubles per block:
@@ -309,9 +494,6 @@ __global__ void kkt_cols_kernel(const double* x, const double* c, const double* 
 
 __global__ void avg_kernel(const double* sum, double inv, int64_t n, double* out) {
   GRID_LOOP(i, n) out[i] = sum[i] * inv;
-}
-__global__ void unscale_kernel(const double* xs, const double* D, int64_t n, double* x, int mul) {
-  GRID_LOOP(i, n) x[i] = mul ? xs[i] * D[i] : xs[i] / D[i];
 }
 __global__ void sq_diff_kernel(const double* a, const double* b, int64_t n, double* part) {
   __shared__ double sh[kB];
@@ -413,6 +595,46 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
     scale_b_kernel<<<grid(m), kB, 0, s>>>(M->rhs.p, S.Dr.p, m, S.b_s.p);
     XE_CUDA(cudaGetLastError());
   }
+  // |b| of the row-normalised problem (KKT denominator), original order
+  double b_l2 = 0.0;
+  {
+    std::vector<double> hb(static_cast<size_t>(m)), hd0(static_cast<size_t>(m));
+    XE_CUDA(cudaMemcpyAsync(hb.data(), M->rhs.p, m * 8, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaMemcpyAsync(hd0.data(), S.Dr0.p, m * 8, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < hb.size(); ++i) b_l2 += (hb[i] * hd0[i]) * (hb[i] * hd0[i]);
+    b_l2 = std::sqrt(b_l2);
+  }
+  // ---- sliced matrices and the sorted index space
+  Sell R, C;
+  sell_plan(M->row_ptr.p, m, R, s);
+  sell_plan(M->col_ptr.p, n, C, s);
+  sell_fill(M->row_ptr.p, M->col.p, S.val_s.p, C.inv.p, R, s);
+  sell_fill(M->col_ptr.p, M->crow.p, S.cval_s.p, R.inv.p, C, s);
+  auto permute = [&](DevBuf<double>& v, const Sell& P, DevBuf<double>& tmp) {
+    gather_kernel<double><<<grid(P.len), kB, 0, s>>>(v.p, P.perm.p, P.len, tmp.p);
+    XE_CUDA(cudaMemcpyAsync(v.p, tmp.p, P.len * 8, cudaMemcpyDeviceToDevice, s));
+  };
+  for (auto* v : {&S.Dr, &S.Dr0, &S.b_s}) permute(*v, R, S.tmpm);
+  for (auto* v : {&S.Dc, &S.c_s, &S.lb_s, &S.ub_s}) permute(*v, C, S.tmpn);
+  DevBuf<int8_t> sense_p;
+  DevBuf<double> obj_p, lb_p;
+  sense_p.alloc(std::max<int64_t>(1, m));
+  obj_p.alloc(std::max<int64_t>(1, n));
+  lb_p.alloc(std::max<int64_t>(1, n));
+  gather_kernel<int8_t><<<grid(m), kB, 0, s>>>(M->sense.p, R.perm.p, m, sense_p.p);
+  gather_kernel<double><<<grid(n), kB, 0, s>>>(M->obj.p, C.perm.p, n, obj_p.p);
+  gather_kernel<double><<<grid(n), kB, 0, s>>>(lb, C.perm.p, n, lb_p.p);
+  XE_CUDA(cudaGetLastError());
+  XE_CUDA(cudaStreamSynchronize(s));
+  S.val_s.release();
+  S.cval_s.release();
+  auto Kmul = [&](const double* xv, double* out) {  // out = K~ x (sorted rows)
+    sell_spmv_kernel<<<items_grid(R), kB, 0, s>>>(view(R), xv, out);
+  };
+  auto KTmul = [&](const double* yv, double* out) {  // out = K~' y (sorted columns)
+    sell_spmv_kernel<<<items_grid(C), kB, 0, s>>>(view(C), yv, out);
+  };
   auto sqdist = [&](const double* a, const double* b, int64_t len) {
     const int g = grid(len);
     sq_diff_kernel<<<g, kB, 0, s>>>(a, b, len, S.part.p);
@@ -433,8 +655,8 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
     normalize_kernel<<<1, kB, 0, s>>>(S.xr.p, S.part.p, 0, n);
     double lam = 0.0;
     for (int it = 0; it < 40; ++it) {
-      spmv_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->col.p, S.val_s.p, S.xr.p, m, S.Kx.p);
-      spmtv_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, S.cval_s.p, S.Kx.p, n, S.xr.p);
+      Kmul(S.xr.p, S.Kx.p);
+      KTmul(S.Kx.p, S.xr.p);
       lam = sqdist(S.xr.p, S.xa.p, n);  // ||K'K v||^2 with |v| = 1
       const int g = grid(n);
       sq_diff_kernel<<<g, kB, 0, s>>>(S.xr.p, S.xa.p, n, S.part.p);
@@ -464,17 +686,13 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   set_step();
 
   Iter it{};
-  it.rp = M->row_ptr.p;
-  it.cp = M->col_ptr.p;
-  it.col = M->col.p;
-  it.row = M->crow.p;
-  it.val = S.val_s.p;
-  it.cval = S.cval_s.p;
+  it.R = view(R);
+  it.C = view(C);
   it.c = S.c_s.p;
   it.lb = S.lb_s.p;
   it.ub = S.ub_s.p;
   it.b = S.b_s.p;
-  it.sense = M->sense.p;
+  it.sense = sense_p.p;
   it.x = S.x.p;
   it.xbar = S.xbar.p;
   it.xsum = S.xsum.p;
@@ -485,16 +703,13 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   it.n = n;
 
   const int block = o.check_every > 0 ? o.check_every : 64;
-  // lanes per column (SpM'V) and per row (SpMV) from the average lengths
-  const int g_col = group_width(n ? static_cast<double>(nnz) / static_cast<double>(n) : 1.0);
-  const int g_row = group_width(m ? static_cast<double>(nnz) / static_cast<double>(m) : 1.0);
   // captured graph of `block` iterations
   cudaGraph_t graph;
   cudaGraphExec_t gexec;
   XE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < block; ++k) {
-    launch_half_step(it, m, n, g_col, s, true);
-    launch_half_step(it, m, n, g_row, s, false);
+    primal_sell_kernel<<<items_grid(C), kB, 0, s>>>(it);
+    dual_sell_kernel<<<items_grid(R), kB, 0, s>>>(it);
   }
   XE_CUDA(cudaStreamEndCapture(s, &graph));
   XE_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
@@ -503,20 +718,12 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   struct Kkt {
     double gap, pres, pobj, dobj, err;
   };
-  std::vector<double> hb(static_cast<size_t>(m)), hd0(static_cast<size_t>(m));
-  XE_CUDA(cudaMemcpyAsync(hb.data(), M->rhs.p, m * 8, cudaMemcpyDeviceToHost, s));
-  XE_CUDA(cudaMemcpyAsync(hd0.data(), S.Dr0.p, m * 8, cudaMemcpyDeviceToHost, s));
-  XE_CUDA(cudaStreamSynchronize(s));
-  double b_l2 = 0.0;
-  for (size_t i = 0; i < hb.size(); ++i) b_l2 += (hb[i] * hd0[i]) * (hb[i] * hd0[i]);
-  b_l2 = std::sqrt(b_l2);
-
   auto kkt = [&](const double* xs, const double* ys) {
-    spmv_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->col.p, S.val_s.p, xs, m, S.Kx.p);
-    spmtv_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, S.cval_s.p, ys, n, S.Kty.p);
+    Kmul(xs, S.Kx.p);
+    KTmul(ys, S.Kty.p);
     const int gm = grid(m), gn = grid(n), g = std::max(gm, gn);
     XE_CUDA(cudaMemsetAsync(S.part.p, 0, static_cast<size_t>(g) * 4 * 8, s));
-    kkt_rows_kernel<<<gm, kB, 0, s>>>(S.Kx.p, S.b_s.p, M->sense.p, ys, S.Dr.p, S.Dr0.p, m, S.part.p);
+    kkt_rows_kernel<<<gm, kB, 0, s>>>(S.Kx.p, S.b_s.p, sense_p.p, ys, S.Dr.p, S.Dr0.p, m, S.part.p);
     kkt_cols_kernel<<<gn, kB, 0, s>>>(xs, S.c_s.p, S.lb_s.p, S.ub_s.p, S.Kty.p, n, S.part.p);
     std::vector<double> h(static_cast<size_t>(g) * 4);
     XE_CUDA(cudaMemcpyAsync(h.data(), S.part.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -610,8 +817,8 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   cudaGraphDestroy(graph);
 
   // certify the prohibitive-cost presolve with the final duals
-  spmtv_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, S.cval_s.p, S.y.p, n, S.Kty.p);
-  certify_kernel<<<grid(n), kB, 0, s>>>(M->obj.p, lb, S.Kty.p, S.Dc.p, n, fixcnt.p + 1);
+  KTmul(S.y.p, S.Kty.p);
+  certify_kernel<<<grid(n), kB, 0, s>>>(obj_p.p, lb_p.p, S.Kty.p, S.Dc.p, n, fixcnt.p + 1);
   unsigned long long fc[2] = {0, 0};
   XE_CUDA(cudaMemcpyAsync(fc, fixcnt.p, 16, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaStreamSynchronize(s));
@@ -628,11 +835,11 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   res->solve_ms = total_ms;
   res->spmv_ms_per_iter = iters ? loop_ms / iters : 0.0;
   if (x_out) {
-    unscale_kernel<<<grid(n), kB, 0, s>>>(S.x.p, S.Dc.p, n, S.tmpn.p, 1);
+    unpermute_scale_kernel<<<grid(n), kB, 0, s>>>(S.x.p, S.Dc.p, C.perm.p, n, S.tmpn.p);
     XE_CUDA(cudaMemcpyAsync(x_out, S.tmpn.p, n * 8, cudaMemcpyDeviceToHost, s));
   }
   if (y_out) {
-    unscale_kernel<<<grid(m), kB, 0, s>>>(S.y.p, S.Dr.p, m, S.tmpm.p, 1);
+    unpermute_scale_kernel<<<grid(m), kB, 0, s>>>(S.y.p, S.Dr.p, R.perm.p, m, S.tmpm.p);
     XE_CUDA(cudaMemcpyAsync(y_out, S.tmpm.p, m * 8, cudaMemcpyDeviceToHost, s));
   }
   XE_CUDA(cudaStreamSynchronize(s));

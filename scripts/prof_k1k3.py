@@ -17,3 +17,8 @@ if which in ("k3", "both"):
     m = xe.build_model(xe.Problem.from_json(configs.vgg16_doc()))
     r = xe.pdhg_solve(m, tol=1e-12, max_iters=int(sys.argv[2]) if len(sys.argv) > 2 else 2048)
     print("k3 vgg16", r.iters, f"{r.ms_per_iter * 1e3:.2f} us/iter", r.primal_obj)
+if which == "k3r":
+    m = xe.build_model(xe.Problem.from_json(configs.resnet50_doc()))
+    print("model", m.n_rows, m.n_cols, m.nnz)
+    r = xe.pdhg_solve(m, tol=1e-12, max_iters=int(sys.argv[2]) if len(sys.argv) > 2 else 2048)
+    print("k3 resnet50", r.iters, f"{r.ms_per_iter * 1e3:.2f} us/iter", r.primal_obj)
