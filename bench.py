@@ -147,7 +147,7 @@ def resnet_pipeline(args):
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    it_bytes = 24 * model.nnz + 56 * (model.n_rows + model.n_cols)
+    it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
     hbm = peaks()[0]
     bpc = prob.cube_words * 4 + 8 + 8 * prob.D + 4
     line = {"metric": METRIC, "value": n / (ms / 1e3), "unit": "candidates/s", "n_gpus": 1, "steps": args.steps,
@@ -405,7 +405,7 @@ def main():
         k1_bytes = 12 * model.nnz + 8 * (model.n_rows + 1) + 26 * model.n_cols
         lp = xe.pdhg_solve(model, tol=1e-7, max_iters=400000)
         want = 118.68224203657523  # HiGHS 1.12.0 on the reference MPS (tests/golden/lp_values.json)
-        it_bytes = 24 * model.nnz + 56 * (model.n_rows + model.n_cols)
+        it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
         line["k1_build"] = {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "ms": build_ms,
                             "achieved_gbs": k1_bytes / (build_ms / 1e3) / 1e9 if build_ms > 0 else None}
         line["pdhg"] = {

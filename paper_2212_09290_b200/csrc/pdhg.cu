@@ -146,7 +146,7 @@ __global__ void scale_b_kernel(const double* b, const double* Dr, int64_t m, dou
 // sptr[s] + 32 t + l) and padded to the slice's longest row (~1 % padding on
 // the configs-2/3 models); the long rows are stored row-major and taken by a
 // whole warp (lanes stride the entries, shuffle reduction), so no lane walks
-// a long row serially (the longest row of ResNet-50 cfg 3 has 435 entries).
+// a long row serially (the longest row of ResNet-50 cfg 3 has 435 entries; threshold below).
 // The solve runs in the reordered index space — vectors permuted once,
 // indices remapped — so every per-row vector access and matrix load is a
 // coalesced 32-lane transaction, and a lane's chain of dependent loads is
@@ -154,8 +154,15 @@ __global__ void scale_b_kernel(const double* b, const double* Dr, int64_t m, dou
 // operands issued before the dot product.  The grouped CSR kernels this
 // replaces (G lanes per row, shuffle reduction) were latency-bound at
 // 1.7 TB/s on ResNet-50 cfg 3 (profiles/r01_k3_resnet_full.txt).
-constexpr int kLong = 12;
 constexpr int kSigma = 1024;
+
+// Rows longer than this take the warp path.  While the slices fit one wave of
+// resident warps (148 SMs x 48) the solve is latency-bound and the longest
+// slice sets the step time, so rows past 12 entries go to warps (VGG-16:
+// 8.8 vs 11.1 us/iteration at 32); with several waves, warps on rows of
+// 13-32 entries waste lanes and throughput rules (ResNet-50 cfg 3: 52.6 vs
+// 82.9 us/iteration at 12).  Measured with scripts/k3_sweep.sh.
+inline int long_threshold(int64_t len) { return (len + 31) / 32 <= 148 * 48 ? 12 : 32; }
 
 struct Sell {
   DevBuf<int64_t> sptr;  // [0, nlong]: long-row offsets; then ns + 1 slice offsets
@@ -174,7 +181,7 @@ struct SellView {
   int64_t len, nlong, ns;
 };
 
-__global__ void sort_key_kernel(const int64_t* p, int64_t n, uint32_t* key, int32_t* iota,
+__global__ void sort_key_kernel(const int64_t* p, int64_t n, int kLong, uint32_t* key, int32_t* iota,
                                 unsigned long long* nlong) {
   GRID_LOOP(i, n) {
     const int64_t len = p[i + 1] - p[i];
@@ -247,7 +254,7 @@ __global__ void unpermute_scale_kernel(const double* in, const double* D, const 
 }
 
 // reorder one dimension of the pattern (p = CSR row or CSC column offsets)
-void sell_plan(const int64_t* p, int64_t n, Sell& S, cudaStream_t s) {
+void sell_plan(const int64_t* p, int64_t n, int long_min, Sell& S, cudaStream_t s) {
   S.len = n;
   const int64_t nn = std::max<int64_t>(1, n);
   DevBuf<uint32_t> key, key_out;
@@ -261,7 +268,7 @@ void sell_plan(const int64_t* p, int64_t n, Sell& S, cudaStream_t s) {
   S.inv.alloc(nn);
   S.slen.alloc(nn);
   XE_CUDA(cudaMemsetAsync(cnt.p, 0, 8, s));
-  sort_key_kernel<<<grid(n), kB, 0, s>>>(p, n, key.p, iota.p, cnt.p);
+  sort_key_kernel<<<grid(n), kB, 0, s>>>(p, n, long_min, key.p, iota.p, cnt.p);
   size_t tmp_bytes = 0;
   XE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key.p, key_out.p, iota.p, S.perm.p,
                                           static_cast<int>(n), 0, 32, s));
@@ -607,8 +614,8 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   }
   // ---- sliced matrices and the sorted index space
   Sell R, C;
-  sell_plan(M->row_ptr.p, m, R, s);
-  sell_plan(M->col_ptr.p, n, C, s);
+  sell_plan(M->row_ptr.p, m, long_threshold(m), R, s);
+  sell_plan(M->col_ptr.p, n, long_threshold(n), C, s);
   sell_fill(M->row_ptr.p, M->col.p, S.val_s.p, C.inv.p, R, s);
   sell_fill(M->col_ptr.p, M->crow.p, S.cval_s.p, R.inv.p, C, s);
   auto permute = [&](DevBuf<double>& v, const Sell& P, DevBuf<double>& tmp) {
