@@ -314,6 +314,17 @@ int xe_round_cubes(const xe_problem* p, const double* x_dev, uint64_t seed, int6
  * optional random bit flip; candidate k a pure function of (seed, first + k). */
 int xe_mutate_cubes(const xe_problem* p, const uint32_t* base_dev, uint64_t seed, int64_t first, int64_t n,
                     int32_t edits, double perturb, uint32_t* cubes_dev, void* stream);
+/* Local-search neighbours in R space: 1..max_moves random moves on the base's
+ * computations R (recompute a parent where one of its consumers is computed;
+ * drop a recomputation; move a computation to another device), then the
+ * canonical saves of the result: each tensor kept on the device of its latest
+ * computation exactly at the steps where it is needed before it is computed
+ * again.  max_moves = 0 returns the base's R with its canonical saves.
+ * n_base bases (independent local-search chains, device [n_base][cube
+ * words]); n a multiple of n_base, candidate k moves base k / (n / n_base).
+ * Candidate k is a pure function of (seed, first + k, its base).  T <= 256. */
+int xe_move_cubes(const xe_problem* p, const uint32_t* base_dev, int64_t n_base, uint64_t seed, int64_t first,
+                  int64_t n, int32_t max_moves, uint32_t* cubes_dev, void* stream);
 /* n uniform random placements dev[n][T] (device buffer): op i on a device
  * that can run it (cost < 1e9), candidate k a pure function of
  * (seed, first + k) — the input family of config 5's placement sweep. */

@@ -231,6 +231,23 @@ def mutate_cubes(problem: Problem, base, n: int, seed: int, first: int = 0, edit
     return out
 
 
+def move_cubes(problem: Problem, base, n: int, seed: int, first: int = 0, max_moves: int = 2, out=None,
+               stream=None):
+    """K4 local search in R space: n neighbours of `base` (int32 CUDA tensor
+    [cube_words], or [n_base, cube_words] for independent chains — n a
+    multiple of n_base, neighbour k of base k // (n // n_base); the S part is
+    ignored): 1..max_moves random moves on the computations, then the
+    canonical saves.  max_moves=0: the base's R with canonical saves."""
+    import torch
+    nb = 1 if base.dim() == 1 else base.shape[0]
+    if out is None:
+        out = torch.empty((n, problem.cube_words), dtype=torch.int32, device=base.device)
+    s = stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.xe_move_cubes(problem.handle, C.c_void_p(base.contiguous().data_ptr()), nb, seed, first, n,
+                            max_moves, C.c_void_p(out.data_ptr()), C.c_void_p(s)))
+    return out
+
+
 def random_placements(problem: Problem, n: int, seed: int, first: int = 0, out=None, stream=None):
     """n uniform random placements (uint8 CUDA tensor [n, T]); candidate k is
     a pure function of (seed, first + k)."""

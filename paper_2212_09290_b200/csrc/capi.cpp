@@ -23,6 +23,8 @@ size_t eval_scratch_bytes(int device);
 void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const uint32_t* cubes,
                        int64_t n, double* obj, int64_t* peak, uint32_t* flags, uint32_t valid_mask,
                        uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
+void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_base, uint64_t seed, int64_t first,
+                       int64_t n, int max_moves, uint32_t* out, cudaStream_t s);
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
                         int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s,
                         const uint32_t* base = nullptr);
@@ -415,6 +417,16 @@ int xe_mutate_cubes(const xe_problem* p, const uint32_t* base_dev, uint64_t seed
     require_uploaded(p);
     round_cubes_device(p, nullptr, seed, first, n, edits, perturb, cubes_dev, static_cast<cudaStream_t>(stream),
                        base_dev);
+  });
+}
+
+int xe_move_cubes(const xe_problem* p, const uint32_t* base_dev, int64_t n_base, uint64_t seed, int64_t first,
+                  int64_t n, int32_t max_moves, uint32_t* cubes_dev, void* stream) {
+  return guard([&] {
+    if (!p || !base_dev || (!cubes_dev && n > 0) || n < 0 || max_moves < 0 || n_base < 1 || n % n_base)
+      fail(XE_ERR_ARG, "bad argument (n must be a multiple of n_base >= 1)");
+    require_uploaded(p);
+    move_cubes_device(p, base_dev, n_base, seed, first, n, max_moves, cubes_dev, static_cast<cudaStream_t>(stream));
   });
 }
 

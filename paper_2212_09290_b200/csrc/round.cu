@@ -228,33 +228,42 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
         const int a1 = lp_dev >= 0 ? a0 : a0 + rng.below(t - a0 + 1);
         int dn = lp_dev >= 0 ? lp_dev : (rng.uniform() < 0.5 ? rng.below(D) : dev[t]);
         if (a.cost[dn * T + i] >= 1.0e9) dn = dev[i];
-        // recompute op v at t on dn, dropping its saves on dev-of-v over
-        // [from, t]; later saves follow it to dn (EQ11 needs a holder at t)
-        auto recompute_at = [&](int v, int from) {
+        // recompute op v at t on device dr, dropping its saves on dev-of-v
+        // over [from, t]; later saves follow it to dr (EQ11 needs a holder at t)
+        auto recompute_at = [&](int v, int from, int dr) {
           const int dv = dev[v];
           for (int tt = from; tt <= t; ++tt) bit_clr(1, dv, tt, v);
-          bit_set(0, dn, t, v);
-          if (dn != dv)
+          bit_set(0, dr, t, v);
+          if (dr != dv)
             for (int tt = t + 1; tt < T; ++tt)
               if (bit_get(1, dv, tt, v)) {
                 bit_clr(1, dv, tt, v);
-                bit_set(1, dn, tt, v);
+                bit_set(1, dr, tt, v);
               }
         };
-        recompute_at(i, a1);
+        recompute_at(i, a1, dn);
         // parents of every op recomputed at t: keep them saved until t, or
-        // (probability 1/2, when dn can run them) recompute them at t too,
-        // dropping their own save windows — chains of recomputation
-        int stack[32], sp = 0;
-        stack[sp++] = i;
+        // (probability 1/2) recompute them at t too, dropping their own save
+        // windows — chains of recomputation.  A recomputed parent runs on its
+        // child's device or (probability 1/4) another one: a chain may cross
+        // devices within the timestep, so a memory-tight device need not hold
+        // the chain's intermediate tensors (config 2's optimum recomputes
+        // ops 0-1 on the cpu and 2-3 on the gpu at t = 39)
+        int stack[32], sdev[32], sp = 0;
+        stack[sp] = i;
+        sdev[sp++] = dn;
         while (sp > 0) {
-          const int v = stack[--sp];
+          --sp;
+          const int v = stack[sp], dvn = sdev[sp];
           for (int k2 = a.in_ptr[v]; k2 < a.in_ptr[v + 1]; ++k2) {
             const int p = a.src[a.in_edge[k2]];
             bool avail = false;
             for (int d = 0; d < D; ++d) avail |= bit_get(0, d, t, p) || bit_get(1, d, t, p);
             if (avail) continue;
-            if (sp < 32 && a.cost[dn * T + p] < 1.0e9 && rng.uniform() < 0.5) {
+            int dr = dvn;
+            if (D > 1 && rng.uniform() < 0.25) dr = (dvn + 1 + rng.below(D - 1)) % D;
+            if (a.cost[dr * T + p] >= 1.0e9) dr = dvn;
+            if (sp < 32 && a.cost[dr * T + p] < 1.0e9 && rng.uniform() < 0.5) {
               // first step after p's last use before t
               int from = p + 1;
               for (int tt = t - 1; tt > p && from == p + 1; --tt)
@@ -267,8 +276,9 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
                     break;
                   }
                 }
-              recompute_at(p, from);
-              stack[sp++] = p;
+              recompute_at(p, from, dr);
+              stack[sp] = p;
+              sdev[sp++] = dr;
               continue;
             }
             const int dp = dev[p];
@@ -318,6 +328,176 @@ __global__ void placement_kernel(const uint8_t* allowed, const uint8_t* n_allowe
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// R-space neighbours with canonical saves (local search over recomputation).
+// A schedule is determined by its computations R; given R, the canonical
+// saves keep each tensor on the device of its latest computation for exactly
+// the steps where it is needed before it is computed again:
+//   hold(u, t)  <=>  next_need(u, t) < next_comp(u, t)
+// with next_need = first step >= t computing a consumer of u (any device) and
+// next_comp = first step >= t computing u (any device).  Saves never move a
+// tensor between devices (EQ11), and a holder beyond these steps only adds
+// memory and copy charges (P = R(dc) and Z(ds), every ds != dc holding u).
+// Moves (Philox keyed by (seed, candidate)): 0..max_moves of
+//   A  recompute u where a consumer v is computed (step and device of one of
+//      v's computations; with probability 1/2 on another device), and with
+//      probability 1/2 its parents there too, recursively (each on the
+//      child's device or, probability 1/4, another): a recomputation chain,
+//   B  drop one recomputation (an R bit off the diagonal),
+//   C  move one computation (any R bit) to another device.
+// max_moves = 0 returns the base with its canonical saves.  Several bases
+// (independent local-search chains): candidate k starts from base
+// k / per_base.
+struct MoveArgs {
+  const double* cost;  // [D][T]
+  const int32_t* src;
+  const int32_t* dst;
+  const int32_t* in_ptr;
+  const int32_t* in_edge;
+  const uint32_t* base;
+  int64_t per_base;
+  int D, T, E, W32;
+  uint64_t seed;
+  int64_t first, n;
+  int max_moves;
+  uint32_t* out;
+};
+
+__global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int D = a.D, T = a.T, W = a.W32;
+  const int words = 2 * D * T * W;
+  uint32_t* cons = reinterpret_cast<uint32_t*>(smem);  // [T][W] consumers of u
+  uint32_t* cube = cons + T * W + wid * (words + T * W);
+  uint32_t* rany = cube + words;  // [T][W] ops computed at t (any device)
+  for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x)
+    atomicOr(&cons[a.src[e] * W + (a.dst[e] >> 5)], 1u << (a.dst[e] & 31));
+  __syncthreads();
+  auto rw = [&](int d, int t, int i) -> uint32_t& { return cube[(d * T + t) * W + (i >> 5)]; };
+  auto rget = [&](int d, int t, int i) -> bool { return (rw(d, t, i) >> (i & 31)) & 1u; };
+
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * kRoundWarps + wid; k < a.n;
+       k += static_cast<int64_t>(gridDim.x) * kRoundWarps) {
+    const uint64_t c = static_cast<uint64_t>(a.first + k);
+    const uint32_t* bc = a.base + static_cast<size_t>(k / a.per_base) * words;
+    for (int i = lane; i < words; i += 32) cube[i] = i < D * T * W ? bc[i] : 0u;
+    __syncwarp();
+    if (lane == 0 && a.max_moves > 0) {
+      Philox rng(a.seed, c, 0x3u);
+      const int nm = 1 + rng.below(a.max_moves);
+      for (int m = 0; m < nm; ++m) {
+        const double u = rng.uniform();
+        if (u < 0.4) {  // A: recompute a parent where its consumer is computed
+          const int e = rng.below(a.E);
+          const int pu = a.src[e], v = a.dst[e];
+          int cnt = 0;
+          for (int d = 0; d < D; ++d)
+            for (int t = v; t < T; ++t) cnt += rget(d, t, v);
+          if (!cnt) continue;
+          int pick = rng.below(cnt), dv = 0, tv = 0;
+          for (int d = 0; d < D && pick >= 0; ++d)
+            for (int t = v; t < T && pick >= 0; ++t)
+              if (rget(d, t, v) && pick-- == 0) dv = d, tv = t;
+          int dr = dv;
+          if (D > 1 && rng.uniform() < 0.5) dr = (dv + 1 + rng.below(D - 1)) % D;
+          if (a.cost[dr * T + pu] >= 1.0e9) dr = dv;
+          if (a.cost[dr * T + pu] >= 1.0e9) continue;
+          rw(dr, tv, pu) |= 1u << (pu & 31);
+          if (rng.uniform() < 0.5) {
+            int stack[32], sdev[32], sp = 0;
+            stack[sp] = pu;
+            sdev[sp++] = dr;
+            while (sp > 0) {
+              --sp;
+              const int x = stack[sp], dx = sdev[sp];
+              for (int q = a.in_ptr[x]; q < a.in_ptr[x + 1]; ++q) {
+                const int pp = a.src[a.in_edge[q]];
+                if (rng.uniform() >= 0.5) continue;
+                int dp = dx;
+                if (D > 1 && rng.uniform() < 0.25) dp = (dx + 1 + rng.below(D - 1)) % D;
+                if (a.cost[dp * T + pp] >= 1.0e9) dp = dx;
+                if (a.cost[dp * T + pp] >= 1.0e9 || rget(dp, tv, pp)) continue;
+                rw(dp, tv, pp) |= 1u << (pp & 31);
+                if (sp < 32) {
+                  stack[sp] = pp;
+                  sdev[sp++] = dp;
+                }
+              }
+            }
+          }
+        } else {  // B / C: pick an R bit (B: off the diagonal)
+          const bool drop = u < 0.65;
+          int cnt = 0;
+          for (int d = 0; d < D; ++d)
+            for (int t = 0; t < T; ++t)
+              for (int w = 0; w < W; ++w) {
+                uint32_t x = rw(d, t, w * 32);
+                if (drop && (t >> 5) == w) x &= ~(1u << (t & 31));
+                cnt += __popc(x);
+              }
+          if (!cnt) continue;
+          int pick = rng.below(cnt), pd = 0, pt = 0, pi = 0;
+          for (int d = 0; d < D && pick >= 0; ++d)
+            for (int t = 0; t < T && pick >= 0; ++t)
+              for (int w = 0; w < W && pick >= 0; ++w) {
+                uint32_t x = rw(d, t, w * 32);
+                if (drop && (t >> 5) == w) x &= ~(1u << (t & 31));
+                const int pc = __popc(x);
+                if (pick < pc) {
+                  for (int q = 0; q < pick; ++q) x &= x - 1;
+                  pd = d, pt = t, pi = w * 32 + __ffs(x) - 1;
+                }
+                pick -= pc;
+              }
+          rw(pd, pt, pi) &= ~(1u << (pi & 31));
+          if (!drop) {
+            int to = pd;
+            if (D > 1) to = (pd + 1 + rng.below(D - 1)) % D;
+            if (a.cost[to * T + pi] >= 1.0e9) to = pd;
+            rw(to, pt, pi) |= 1u << (pi & 31);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // canonical saves
+    for (int i = lane; i < T * W; i += 32) {
+      const int t = i / W, w = i % W;
+      uint32_t x = 0u;
+      for (int d = 0; d < D; ++d) x |= cube[(d * T + t) * W + w];
+      rany[i] = x;
+    }
+    __syncwarp();
+    for (int u = lane; u < T; u += 32) {
+      uint32_t hold[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      int nn = T, nc = T;
+      for (int t = T - 1; t >= 0; --t) {
+        bool need = false;
+        for (int w = 0; w < W; ++w) need |= (rany[t * W + w] & cons[u * W + w]) != 0u;
+        if ((rany[t * W + (u >> 5)] >> (u & 31)) & 1u) nc = t;
+        if (need) nn = t;
+        if (nn < nc) hold[t >> 5] |= 1u << (t & 31);
+      }
+      int hd = -1;
+      for (int t = 0; t < T; ++t) {
+        if ((rany[t * W + (u >> 5)] >> (u & 31)) & 1u) {
+          for (int d = D - 1; d >= 0; --d)
+            if (rget(d, t, u)) hd = d;
+        } else if (hd >= 0 && ((hold[t >> 5] >> (t & 31)) & 1u)) {
+          atomicOr(&cube[((D + hd) * T + t) * W + (u >> 5)], 1u << (u & 31));
+        }
+      }
+    }
+    __syncwarp();
+    uint32_t* out = a.out + static_cast<size_t>(k) * words;
+    for (int i = lane; i < words; i += 32) out[i] = cube[i];
+    __syncwarp();
+  }
+}
 }  // namespace
 
 void random_placements_device(const xe_problem* pr, uint64_t seed, int64_t first, int64_t n, uint8_t* out,
@@ -414,6 +594,43 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     XE_CUDA(cudaGetLastError());
   }
   if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));  // the recompute list above is call-local
+}
+
+void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_base, uint64_t seed, int64_t first,
+                       int64_t n, int max_moves, uint32_t* out, cudaStream_t s) {
+  const HostProblem& h = pr->h;
+  if (h.T > 256) fail(XE_ERR_TOO_LARGE, "R-space moves support T <= 256");
+  MoveArgs a{};
+  a.cost = pr->d_cost.p;
+  a.src = pr->d_src.p;
+  a.dst = pr->d_dst.p;
+  a.in_ptr = pr->d_in_ptr.p;
+  a.in_edge = pr->d_in_edge.p;
+  a.base = base;
+  a.per_base = std::max<int64_t>(1, n / std::max<int64_t>(1, n_base));
+  a.D = h.D;
+  a.T = h.T;
+  a.E = h.E;
+  a.W32 = (h.T + 31) / 32;
+  a.seed = seed;
+  a.first = first;
+  a.n = n;
+  a.max_moves = max_moves;
+  a.out = out;
+  const int words = 2 * h.D * h.T * a.W32;
+  const int smem = (h.T * a.W32 + kRoundWarps * (words + h.T * a.W32)) * 4;
+  int limit = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
+  if (smem > limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the move kernel");
+  XE_CUDA(cudaFuncSetAttribute(move_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int nsm = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+  const int64_t want = (n + kRoundWarps - 1) / kRoundWarps;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, nsm * 16)));
+  if (n > 0) {
+    move_kernel<<<grid, kRoundWarps * 32, smem, s>>>(a);
+    XE_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace xe

@@ -8,7 +8,7 @@ Outputs (committed, small):
   tests/golden/f1_golden.mps     write_mps(build_model(chain3)); checked equal
                                  to proj/tests/data/f1_golden.mps at generation
   tests/golden/mps_sha256.json   sha256/length of write_mps for fixtures x
-                                 options and the VGG-16 / ResNet-50 configs
+                                 options and the VGG-16 / ResNet-50 / U-Net configs
   tests/golden/eval_*.npz        seeded candidates + reference obj/peaks/flags
   tests/golden/pins.json         solve_exact / assignment_oracle optima, LP values
 """
@@ -99,7 +99,7 @@ def main():
             for quad in (0, 1):
                 for en in ((0, 1) if a.energy is not None else (0,)):
                     mps[f"{fx}/s{strict}q{quad}e{en}"] = sha(rp.write_mps(strict, quad, en))
-    for cfg in ("vgg16", "resnet50"):
+    for cfg in ("vgg16", "resnet50", "unet"):
         rp = R.load(configs.CONFIGS[cfg]())
         for strict in (0, 1):
             mps[f"{cfg}/s{strict}q0e0"] = sha(rp.write_mps(strict, 0, 0))

@@ -5,7 +5,9 @@ for the K3 parity tests -> tests/golden/lp_values.json.
 The model is the oracle's CSR (pinned byte-for-byte to the reference's
 write_mps, tests/test_oracle_cpu.py); binaries relaxed to [0,1], FX 0, U in
 [0, budget], P in [0,1].  Third-party solver: HiGHS 1.12.0 inside SciPy 1.18.1.
-Usage: python scripts/gen_lp_golden.py [--big]   (--big adds ResNet-50 cfg3, ~11 min IPM)
+Usage: python scripts/gen_lp_golden.py [--big] [--unet]
+  --big adds ResNet-50 cfg 3 (~11 min IPM); --unet computes only U-Net cfg 4
+  (IPM) and merges it into the existing file.
 """
 import json
 import os
@@ -67,6 +69,12 @@ def main():
     cases["chain_lowmem@25"] = (lm.with_budgets([full * 25 // 100]), False, False)
     for s in range(1, 6):
         cases[f"rand{s}"] = (xo.arrays_from_json(configs.random_small_doc(s)), False, False)
+    if "--unet" in sys.argv:
+        cases = {}
+        a = xo.arrays_from_json(configs.unet_doc())
+        v, dt = lp_value(a, method="highs-ipm")
+        out["unet"] = {"lp": v, "seconds": dt, "method": "highs-ipm"}
+        print("unet", v, dt, flush=True)
     for k, (a, strict, en) in cases.items():
         v, dt = lp_value(a, strict, en)
         out[k] = {"lp": v, "seconds": dt}

@@ -35,6 +35,8 @@ def problem(name):
         return xe.Problem.from_json(configs.random_small_doc(int(name[4:])))
     if name == "resnet50":
         return xe.Problem.from_json(configs.resnet50_doc())
+    if name == "unet":
+        return xe.Problem.from_json(configs.unet_doc())
     raise KeyError(name)
 
 
@@ -71,10 +73,11 @@ def test_bound_overrides_fix_a_node():
     assert node.primal_obj >= base.primal_obj - 1e-6
 
 
-@pytest.mark.skipif("resnet50" not in LP, reason="run scripts/gen_lp_golden.py --big")
-def test_resnet50_lp():
-    want = LP["resnet50"]["lp"]
-    m = xe.build_model(problem("resnet50"))
+@pytest.mark.parametrize("name", ["resnet50", "unet"])
+def test_large_lp(name):
+    # configs 3 and 4 (HiGHS IPM goldens: scripts/gen_lp_golden.py --big / --unet)
+    want = LP[name]["lp"]
+    m = xe.build_model(problem(name))
     r = xe.pdhg_solve(m, tol=1e-7, max_iters=1000000)
     assert r.certified
     assert abs(r.primal_obj - want) <= 1e-5 * abs(want), (r.primal_obj, want, r.iters)

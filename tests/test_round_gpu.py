@@ -72,3 +72,84 @@ def test_local_search_neighbours(oracle):
     r = xe.evaluate_cubes(prob, nb)
     assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
     assert np.array_equal(r.peak.cpu().numpy(), p)
+
+
+def canonical_saves_numpy(a, R):
+    """Restatement of the canonical saves (xe_move_cubes): tensor u kept on
+    the (lowest) device of its latest computation at every step t where its
+    next need (a consumer computed, any device) comes before its next
+    computation."""
+    D, T = a.D, a.T
+    cons = [[] for _ in range(T)]
+    for s_, d_ in zip(a.src, a.dst):
+        cons[s_].append(d_)
+    comp = R.any(axis=0)  # [t][i]
+    S = np.zeros_like(R)
+    for u in range(T):
+        need = comp[:, cons[u]].any(axis=1) if cons[u] else np.zeros(T, bool)
+        nn = nc = T
+        hold = np.zeros(T, bool)
+        for t in range(T - 1, -1, -1):
+            if comp[t, u]:
+                nc = t
+            if need[t]:
+                nn = t
+            hold[t] = nn < nc
+        hd = -1
+        for t in range(T):
+            if comp[t, u]:
+                hd = int(np.flatnonzero(R[:, t, u])[0])
+            elif hd >= 0 and hold[t]:
+                S[hd, t, u] = True
+    return S
+
+
+@pytest.mark.parametrize("name", ["fig2", "vgg16", "resnet50"])
+def test_move_cubes_canonical_saves(oracle, name):
+    from cubegen import unpack
+    text = golden_problem_text(name) if name == "fig2" else configs.CONFIGS[name]()
+    a = xo.arrays_from_json(text)
+    prob = xe.Problem.from_json(text)
+    n = 32 if name == "resnet50" else 200
+    base = xe.round_cubes(prob, n, seed=3, edits=4, perturb=0.0)
+    canon = xe.move_cubes(prob, base, n, 0, max_moves=0)
+    c = canon.cpu().numpy().view(np.uint32)
+    R0, _ = unpack(base.cpu().numpy().view(np.uint32), a.D, a.T)
+    R, S = unpack(c, a.D, a.T)
+    assert np.array_equal(R, R0)  # no move: computations unchanged
+    for k in range(n):
+        assert np.array_equal(S[k], canonical_saves_numpy(a, R[k])), k
+    # idempotent, and the K2 evaluation of canonical cubes matches the oracle bit for bit
+    assert torch.equal(xe.move_cubes(prob, canon, n, 0, max_moves=0), canon)
+    o, p, f = oracle.eval_cubes(a, c)
+    r = xe.evaluate_cubes(prob, canon, valid_mask=0)
+    assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
+    assert np.array_equal(r.peak.cpu().numpy(), p)
+    assert np.array_equal(r.flags.cpu().numpy().astype(np.uint32), f)
+    # the rounding's structural validity survives (holders exist where needed)
+    assert ((f & STRUCTURAL) == 0).all()
+
+
+def test_move_cubes_neighbours(oracle):
+    from cubegen import unpack
+    a = xo.arrays_from_json(configs.vgg16_doc())
+    prob = xe.Problem.from_json(configs.vgg16_doc())
+    bases = xe.move_cubes(prob, xe.round_cubes(prob, 4, seed=9, edits=3, perturb=0.0), 4, 0, max_moves=0)
+    nb = xe.move_cubes(prob, bases, 4 * 256, 21, first=0, max_moves=3)
+    # pure function of (seed, index, base); chains map to blocks of 256
+    assert torch.equal(nb, xe.move_cubes(prob, bases, 4 * 256, 21, first=0, max_moves=3))
+    R, S = unpack(nb.cpu().numpy().view(np.uint32), a.D, a.T)
+    Rb, _ = unpack(bases.cpu().numpy().view(np.uint32), a.D, a.T)
+    changed = 0
+    for k in range(nb.shape[0]):
+        diff = int((R[k] != Rb[k // 256]).sum())
+        changed += diff > 0
+        assert np.array_equal(S[k], canonical_saves_numpy(a, R[k]))
+    assert changed > 0.8 * nb.shape[0]
+    # neighbours keep one diagonal computation per step and no R above the diagonal
+    assert (R[:, :, np.arange(a.T), np.arange(a.T)].sum(axis=1) == 1).all()
+    assert not np.triu(np.ones((a.T, a.T), bool), 1)[None, None].__and__(R).any()
+    o, p, f = oracle.eval_cubes(a, nb.cpu().numpy().view(np.uint32), strict=True)
+    r = xe.evaluate_cubes(prob, nb, xe.ModelOptions(strict_free=True), valid_mask=0)
+    assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
+    assert np.array_equal(r.flags.cpu().numpy().astype(np.uint32), f)

@@ -4,7 +4,10 @@ config 1 (the reference's own pins, proj/tests/test_solver.cpp):
   F1 chain3 9.0 (:66-86), 8 MiB -> 9.0, 3 MiB infeasible (:88-97),
   F2 fig2 11.0 (:99-119),
   F3 chain_lowmem sweep 24, 24, 24, 24, 27 at 100/65/50/35/25 % and
-  10 MiB -> 24, 9/8 MiB -> 27, 4 MiB - 1 infeasible (:121-153)."""
+  10 MiB -> 24, 9/8 MiB -> 27, 4 MiB - 1 infeasible (:121-153);
+and config 2 (VGG-16, strict_free): the reference's MILP optimum
+128.32908933333337 with peaks cpu 26,894,336 / gpu 60,411,904 B (HiGHS via
+solve_external)."""
 import numpy as np
 import pytest
 
@@ -62,3 +65,29 @@ def test_chain_lowmem_boundaries(budget, want):
 def test_chain_lowmem_infeasible_below_largest_tensor():
     r = search(prob("chain_lowmem", 4 * MiB - 1), n_per_round=1 << 14, rounds=1, use_lp=False)
     assert r.index == -1
+
+
+VGG_OPT = 128.32908933333337
+VGG_PEAKS = [26894336, 60411904]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_vgg16_reaches_reference_milp_optimum(seed):
+    from bench import configs
+    p = xe.Problem.from_json(configs.vgg16_doc())
+    r = search(p, xe.ModelOptions(strict_free=True), n_per_round=1 << 20, rounds=2, edits=6, seed=seed)
+    assert r.objective == VGG_OPT, (r.objective, r.rounding_objective)
+    assert r.peaks.tolist() == VGG_PEAKS
+    assert r.lp_bound <= VGG_OPT
+    # the incumbent re-scored by the oracle (pinned to the reference): same bits, valid
+    from oracle import xo
+    from paper_2212_09290_b200.search import DEFAULT_MASK
+    a = xo.arrays_from_json(configs.vgg16_doc())
+    obj, peak, flags = xo.Oracle().eval_cubes(a, r.cube[None], strict=True)
+    assert obj[0] == VGG_OPT and peak[0].tolist() == VGG_PEAKS and (int(flags[0]) & DEFAULT_MASK) == 0
+
+
+def test_local_search_off_is_rounding_only():
+    p = prob("fig2")
+    r = search(p, n_per_round=1 << 14, rounds=1, chains=0)
+    assert r.ls_improvements == 0 and r.objective == r.rounding_objective
