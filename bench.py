@@ -251,6 +251,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-pdhg", action="store_true")
+    ap.add_argument("--skip-search", action="store_true")
     ap.add_argument("--workload", default="vgg16", choices=["vgg16", "random2000", "resnet50"],
                     help="vgg16: BASELINE config 2 (the headline); random2000: config 5 placement sweep; "
                          "resnet50: config 3 (K1 + PDHG LP + LP-guided rounding + evaluation)")
@@ -418,6 +419,24 @@ def main():
                          "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9 if lp.ms_per_iter > 0 else None,
                          "peak": hbm_gbs, "unit": "GB/s"},
         }
+
+    # ---- the search on the same config: time to the reference's MILP optimum ----
+    if rank == 0 and not args.skip_search:
+        import time
+        from paper_2212_09290_b200.search import search
+        opt = 128.32908933333337  # reference solve_external (HiGHS MILP, 86 s on the host), SURVEY §8c
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sr = search(prob, xe.ModelOptions(strict_free=True), n_per_round=1 << 20, rounds=2, edits=6, seed=1)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        line["search"] = {
+            "workload": "vgg16 cfg2 strict_free best schedule: K1 -> K3 LP -> K4 rounding + R-space local-search "
+                        "population -> K2 exact scoring (wall clock, one GPU)",
+            "objective": sr.objective, "reference_milp_optimum": opt, "equal_to_reference": sr.objective == opt,
+            "peaks": [int(v) for v in sr.peaks] if sr.peaks is not None else None,
+            "reference_peaks": [26894336, 60411904], "lp_bound": sr.lp_bound, "rounding_objective": sr.rounding_objective,
+            "candidates_evaluated": sr.n_evaluated, "seconds": dt, "reference_seconds": 86.0}
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     if rank == 0 and world == 1 and not args.skip_cpu:
