@@ -422,7 +422,6 @@ def main():
 
     # ---- the search on the same config: time to the reference's MILP optimum ----
     if rank == 0 and not args.skip_search:
-        import time
         from paper_2212_09290_b200.search import search
         opt = 128.32908933333337  # reference solve_external (HiGHS MILP, 86 s on the host), SURVEY §8c
         torch.cuda.synchronize()
