@@ -331,6 +331,50 @@ int xe_move_cubes(const xe_problem* p, const uint32_t* base_dev, int64_t n_base,
 int xe_random_placements(const xe_problem* p, uint64_t seed, int64_t first, int64_t n, uint8_t* dev_out,
                          void* stream);
 
+/* ---- best-schedule search (K1 -> K3 -> K4 -> K2, one native call) ------
+ * The GPU counterpart of solve_exact / solve_external (solver.hpp:49-58):
+ * LP relaxation (PDHG), LP-guided rounding with canonical saves, exact K2
+ * scoring, then a population of R-space local searches (xe_move_cubes).
+ * Valid = (flags & valid_mask) == 0.  The rounding incumbent is the first
+ * minimum in global index order (solver.cpp:57-61); the local search
+ * replaces it only when strictly better.  Sharding: rounding block r of rank
+ * k is at global index first + (r*world + k)*n_per_round; the local-search
+ * seed is (seed, rank); exchanging the per-rank results is the caller's. */
+typedef struct xe_search_opts {
+  int64_t n_per_round;   /* rounded candidates per round (default 1<<18) */
+  int32_t rounds;        /* default 4 */
+  int32_t edits;         /* drop-and-recompute edits per rounded candidate (3) */
+  uint64_t seed;         /* default 1 */
+  int32_t use_lp;        /* 1: LP-guided rounding, LP bound reported (default 1) */
+  double lp_tol;         /* PDHG relative tolerance (1e-6) */
+  uint32_t valid_mask;   /* default XE_F_CHECK_MASK | XE_F_BUDGET | XE_F_DECODE */
+  int32_t canonical;     /* 1: canonical saves on rounded candidates (default 1, T <= 256) */
+  int32_t chains;        /* local-search population (256; 0 = rounding only) */
+  int32_t chain_n;       /* neighbours per chain per iteration (1024) */
+  int32_t chain_iters;   /* iterations (100) */
+  int32_t max_moves;     /* moves per neighbour, 1..max_moves (4) */
+  int32_t stall;         /* iterations without improvement before a kick (15) */
+  int64_t first;         /* global index of the first rounded candidate (0) */
+  int32_t rank, world;   /* candidate sharding (0, 1) */
+} xe_search_opts;
+
+typedef struct xe_search_result {
+  double objective;           /* best valid objective found (inf: none) */
+  double rounding_objective;  /* best rounding candidate alone */
+  int64_t index;              /* its global index (-1: no valid candidate) */
+  double lp_bound;            /* LP relaxation value (NaN without LP) */
+  int32_t has_lp, lp_certified;
+  int64_t n_evaluated, n_valid; /* candidates scored; valid rounding candidates */
+  int32_t improvements;       /* local-search improvements of the incumbent */
+  int32_t reserved;
+} xe_search_result;
+
+void xe_search_opts_default(xe_search_opts* o);
+/* cube_host: [cube words] canonical (R, S) cube of the best schedule, or
+ * NULL; peaks_host: [D] its per-device peaks, or NULL. */
+int xe_search(const xe_problem* p, const xe_model_opts* opts, const xe_search_opts* so, xe_search_result* res,
+              uint32_t* cube_host, int64_t* peaks_host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

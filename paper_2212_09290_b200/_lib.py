@@ -112,6 +112,21 @@ class PdhgResult(C.Structure):
                 ("presolve_fixed", C.c_int32), ("certified", C.c_int32)]
 
 
+class SearchOpts(C.Structure):
+    _fields_ = [("n_per_round", C.c_int64), ("rounds", C.c_int32), ("edits", C.c_int32),
+                ("seed", C.c_uint64), ("use_lp", C.c_int32), ("lp_tol", C.c_double),
+                ("valid_mask", C.c_uint32), ("canonical", C.c_int32), ("chains", C.c_int32),
+                ("chain_n", C.c_int32), ("chain_iters", C.c_int32), ("max_moves", C.c_int32),
+                ("stall", C.c_int32), ("first", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32)]
+
+
+class SearchResult(C.Structure):
+    _fields_ = [("objective", C.c_double), ("rounding_objective", C.c_double), ("index", C.c_int64),
+                ("lp_bound", C.c_double), ("has_lp", C.c_int32), ("lp_certified", C.c_int32),
+                ("n_evaluated", C.c_int64), ("n_valid", C.c_int64), ("improvements", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 # symbol -> (restype, argtypes); the set of exports include/xengine_b200.h declares
 P = C.c_void_p
 SIGNATURES = {
@@ -150,6 +165,8 @@ SIGNATURES = {
                                      C.POINTER(Best), P]),
     "xe_assignment_oracle": (C.c_int, [P, C.POINTER(C.c_double), P, C.POINTER(C.c_int64)]),
     "xe_pdhg_solve": (C.c_int, [P, C.POINTER(PdhgOpts), C.POINTER(PdhgResult), P, P]),
+    "xe_search_opts_default": (None, [C.POINTER(SearchOpts)]),
+    "xe_search": (C.c_int, [P, P, C.POINTER(SearchOpts), C.POINTER(SearchResult), P, P, P]),
     "xe_mutate_cubes": (C.c_int, [P, P, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_double, P, P]),
     "xe_move_cubes": (C.c_int, [P, P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, P, P]),
     "xe_random_placements": (C.c_int, [P, C.c_uint64, C.c_int64, C.c_int64, P, P]),
