@@ -3,8 +3,10 @@
 // Placement solvers (drop-in for proj/include/xengine/solver.hpp:13-40).
 //   save_all_assignment  save-all (R, S) cubes of a placement, completed on the GPU
 //   assignment_oracle    the full D^T placement sweep as one GPU launch (K2b)
-// solve_exact / solve_external (memoised DFS, MPS file bridge) are outside
-// the B200 hot path.
+//   solve_search         the GPU best-schedule search (xe_search), in place of
+//                        solve_exact / solve_external (solver.hpp:42-58)
+// solve_exact / solve_external themselves (memoised DFS, MPS file bridge) are
+// outside the B200 hot path.
 #pragma once
 
 #include <cstdint>
@@ -35,5 +37,29 @@ struct Solution {
 
 Assignment save_all_assignment(const Problem& p, const std::vector<int>& devices);
 Solution assignment_oracle(const Problem& p);
+
+// Parameters of solve_search (xe_search_opts in include/xengine_b200.h).
+struct SearchParams {
+  std::int64_t candidates_per_round = 1 << 18;
+  int rounds = 4;
+  int edits = 3;            // drop-and-recompute edits per rounded candidate
+  std::uint64_t seed = 1;
+  bool use_lp = true;       // LP-guided rounding and the LP lower bound
+  int chains = 256;         // local-search population (0: rounding only)
+  int chain_neighbours = 1024;
+  int chain_iters = 100;
+  int max_moves = 4;
+  int stall = 15;
+};
+
+// Best schedule by the GPU search: K1 model -> K3 LP relaxation -> K4
+// rounding with canonical saves -> K2 exact scoring (objective_value of the
+// completion, check_assignment, integer budgets, decode legality) -> R-space
+// local-search population.  backend "b200"; status Optimal when the
+// objective meets the LP lower bound (to 1e-9 relative), LimitReached
+// otherwise (objective NaN and an empty assignment when no valid schedule
+// was found: infeasibility is not proven); nodes_explored = candidates
+// scored.  The assignment is complete_assignment of the best (R, S).
+Solution solve_search(const Problem& p, const ModelOptions& opts = {}, const SearchParams& params = {});
 
 }  // namespace xengine

@@ -907,4 +907,49 @@ Solution assignment_oracle(const Problem& p) {
   return s;
 }
 
+Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchParams& params) {
+  validate_problem(p);
+  const int D = p.device_count(), T = p.op_count();
+  Handle h = upload(describe(p, opts.energy));
+  xe_search_opts so;
+  xe_search_opts_default(&so);
+  so.n_per_round = params.candidates_per_round;
+  so.rounds = params.rounds;
+  so.edits = params.edits;
+  so.seed = params.seed;
+  so.use_lp = params.use_lp ? 1 : 0;
+  so.chains = params.chains;
+  so.chain_n = params.chain_neighbours;
+  so.chain_iters = params.chain_iters;
+  so.max_moves = params.max_moves;
+  so.stall = params.stall;
+  const xe_model_opts o = c_opts(opts);
+  xe_search_result r{};
+  std::vector<uint32_t> cube(xe_cube_bytes(D, T) / 4);
+  std::vector<int64_t> peaks(static_cast<size_t>(D));
+  ck(xe_search(h.get(), &o, &so, &r, cube.data(), peaks.data(), nullptr));
+  Solution s;
+  s.backend = "b200";
+  s.nodes_explored = r.n_evaluated;
+  if (r.index < 0) {
+    s.status = SolveStatus::LimitReached;
+    s.objective_ms = std::numeric_limits<double>::quiet_NaN();
+    return s;
+  }
+  const bool proven = r.has_lp && r.objective <= r.lp_bound + 1e-9 * std::max(1.0, std::fabs(r.objective));
+  s.status = proven ? SolveStatus::Optimal : SolveStatus::LimitReached;
+  s.objective_ms = r.objective;
+  BitCube R(D, T), S(D, T);
+  const int W = (T + 31) / 32;
+  for (int which = 0; which < 2; ++which)
+    for (int d = 0; d < D; ++d)
+      for (int t = 0; t < T; ++t)
+        for (int i = 0; i < T; ++i)
+          if ((cube[((static_cast<size_t>(which) * D + d) * T + t) * W + i / 32] >> (i % 32)) & 1u)
+            (which ? S : R).at(d, t, i) = 1;
+  s.assignment = complete_assignment(p, opts, R, S);
+  s.assignment.objective_reported = r.objective;
+  return s;
+}
+
 }  // namespace xengine

@@ -389,6 +389,44 @@ void device_cases() {
     CHECK(s.assignment.objective_reported == 11.0);
     CHECK(check_assignment(build_model(p), s.assignment).empty());
   });
+  run("solve_search: F1 chain3 = 9.0, proven by the LP bound", [] {
+    Problem p = fixture("chain3");
+    SearchParams sp;
+    sp.candidates_per_round = 1 << 14;
+    sp.rounds = 2;
+    sp.chain_iters = 10;
+    Solution s = solve_search(p, {}, sp);
+    CHECK(s.backend == "b200");
+    CHECK(s.objective_ms == 9.0);
+    CHECK(s.status == SolveStatus::Optimal);
+    CHECK(s.assignment.objective_reported == 9.0);
+    CHECK(objective_value(s.assignment, p) == 9.0);
+    CHECK(check_assignment(build_model(p), s.assignment).empty());
+    CHECK(s.nodes_explored > 0);
+  });
+  run("solve_search: F2 fig2 = 11.0 (LP bound 9.83: not proven)", [] {
+    Problem p = fixture("fig2");
+    SearchParams sp;
+    sp.candidates_per_round = 1 << 15;
+    sp.rounds = 2;
+    sp.chain_iters = 20;
+    Solution s = solve_search(p, {}, sp);
+    CHECK(s.objective_ms == 11.0);
+    CHECK(s.status == SolveStatus::LimitReached);
+    CHECK(objective_value(s.assignment, p) == 11.0);
+    CHECK(check_assignment(build_model(p), s.assignment).empty());
+  });
+  run("solve_search: F1 at 3 MiB has no valid schedule", [] {
+    Problem p = with_budgets(fixture("chain3"), {3 * kMiB});
+    SearchParams sp;
+    sp.candidates_per_round = 1 << 12;
+    sp.rounds = 1;
+    sp.use_lp = false;
+    Solution s = solve_search(p, {}, sp);
+    CHECK(s.status == SolveStatus::LimitReached);
+    CHECK(std::isnan(s.objective_ms));
+    CHECK(s.assignment.values.empty());
+  });
   run("batched evaluation agrees with the map API", [] {
     Problem p = fixture("fig2");
     std::vector<std::pair<BitCube, BitCube>> cands;
