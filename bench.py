@@ -190,9 +190,11 @@ def placement_sweep(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from bench.dist import init_dist
+        local = init_dist(local)
+    else:
+        torch.cuda.set_device(local)
     prob = xe.Problem.from_json(configs.random2000_doc(), device=local)
     n = min(args.n, 4_000_000)
     dev = xe.random_placements(prob, n, SEED, first=rank * n)
@@ -269,9 +271,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from bench.dist import init_dist
+        local = init_dist(local)
+    else:
+        torch.cuda.set_device(local)
 
     import paper_2212_09290_b200 as xe
     from paper_2212_09290_b200 import _lib
