@@ -348,7 +348,8 @@ typedef struct xe_search_opts {
   int32_t use_lp;        /* 1: LP-guided rounding, LP bound reported (default 1) */
   double lp_tol;         /* PDHG relative tolerance (1e-6) */
   uint32_t valid_mask;   /* default XE_F_CHECK_MASK | XE_F_BUDGET | XE_F_DECODE */
-  int32_t canonical;     /* 1: canonical saves on rounded candidates (default 1, T <= 256) */
+  int32_t canonical;     /* 1: canonical saves on rounded candidates (default 1; both this and the
+                            local search are skipped when a cube does not fit the move kernel) */
   int32_t chains;        /* local-search population (256; 0 = rounding only) */
   int32_t chain_n;       /* neighbours per chain per iteration (1024) */
   int32_t chain_iters;   /* iterations (100) */

@@ -596,6 +596,19 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));  // the recompute list above is call-local
 }
 
+// shared memory of the move kernel: consumer masks + per warp a cube and the
+// ops-computed-at-t rows
+int move_smem_bytes(const HostProblem& h) {
+  const int W = (h.T + 31) / 32, words = 2 * h.D * h.T * W;
+  return (h.T * W + kRoundWarps * (words + h.T * W)) * 4;
+}
+
+bool move_supported(const xe_problem* pr) {
+  int limit = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
+  return pr->h.T <= 256 && move_smem_bytes(pr->h) <= limit;
+}
+
 void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_base, uint64_t seed, int64_t first,
                        int64_t n, int max_moves, uint32_t* out, cudaStream_t s) {
   const HostProblem& h = pr->h;
@@ -617,8 +630,7 @@ void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_bas
   a.n = n;
   a.max_moves = max_moves;
   a.out = out;
-  const int words = 2 * h.D * h.T * a.W32;
-  const int smem = (h.T * a.W32 + kRoundWarps * (words + h.T * a.W32)) * 4;
+  const int smem = move_smem_bytes(h);
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
   if (smem > limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the move kernel");

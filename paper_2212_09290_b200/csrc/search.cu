@@ -29,6 +29,7 @@
 #include "csr.hpp"
 
 namespace xe {
+bool move_supported(const xe_problem* pr);  // round.cu
 namespace {
 
 // best valid neighbour of every chain: one warp per chain, lowest index on ties
@@ -98,7 +99,7 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
                    uint32_t* cube_host, int64_t* peaks_host, cudaStream_t s) {
   const HostProblem& h = pr->h;
   const int words = 2 * h.D * h.T * ((h.T + 31) / 32);
-  const bool movable = h.T <= 256;
+  const bool movable = move_supported(pr);  // the move kernel's cube fits shared memory
   const bool canonical = so.canonical && movable;
   const int chains = movable ? so.chains : 0;
   const uint32_t mask = so.valid_mask;
