@@ -360,7 +360,8 @@ typedef struct xe_search_opts {
 } xe_search_opts;
 
 typedef struct xe_search_result {
-  double objective;           /* best valid objective found (inf: none) */
+  double objective;           /* best valid objective found (inf: none; may be finite with index -1:
+                                 the local search reached feasibility from over-budget candidates) */
   double rounding_objective;  /* best rounding candidate alone */
   int64_t index;              /* its global index (-1: no valid candidate) */
   double lp_bound;            /* LP relaxation value (NaN without LP) */

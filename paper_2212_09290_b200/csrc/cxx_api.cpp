@@ -931,7 +931,7 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
   Solution s;
   s.backend = "b200";
   s.nodes_explored = r.n_evaluated;
-  if (r.index < 0) {
+  if (!std::isfinite(r.objective)) {
     s.status = SolveStatus::LimitReached;
     s.objective_ms = std::numeric_limits<double>::quiet_NaN();
     return s;

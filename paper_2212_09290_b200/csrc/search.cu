@@ -19,8 +19,13 @@
 //              best `chains` distinct objectives as the starting population
 //   local search: each iteration evaluates `chain_n` neighbours of every
 //              chain (1..max_moves R-space moves + canonical saves), a chain
-//              moves to its best valid neighbour when it improves, or after
+//              moves to its best neighbour when it improves, or after
 //              `stall` iterations without improvement (a kick)
+// Scores: a valid schedule scores its objective; one that fails only on
+// memory (BUDGET / U_BOUND) scores kOverBudget + its relative excess
+// sum_d max(0, peak_d - b_d) / b_d, so chains seeded from over-budget
+// candidates (tight budgets where the rounding finds no valid schedule)
+// first descend to feasibility; anything else is never accepted.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -32,8 +37,22 @@ namespace xe {
 bool move_supported(const xe_problem* pr);  // round.cu
 namespace {
 
-// best valid neighbour of every chain: one warp per chain, lowest index on ties
+constexpr double kOverBudget = 1e200;  // above any schedule's objective
+constexpr uint32_t kMemFlags = XE_F_BUDGET | XE_F_U_BOUND;
+
+__host__ __device__ inline double score(double obj, uint32_t flags, uint32_t mask, const int64_t* peak,
+                                        const int64_t* budget, int D) {
+  if ((flags & mask) == 0u) return obj;
+  if ((flags & mask & ~kMemFlags) != 0u) return INFINITY;
+  double ex = 0.0;
+  for (int d = 0; d < D; ++d)
+    if (peak[d] > budget[d]) ex += static_cast<double>(peak[d] - budget[d]) / static_cast<double>(budget[d] > 0 ? budget[d] : 1);
+  return kOverBudget + ex;
+}
+
+// best-scoring neighbour of every chain: one warp per chain, lowest index on ties
 __global__ void chain_select_kernel(const double* __restrict__ obj, const uint32_t* __restrict__ flags,
+                                    const int64_t* __restrict__ peak, const int64_t* __restrict__ budget, int D,
                                     uint32_t mask, int P, int M, double* __restrict__ vbest,
                                     int32_t* __restrict__ jbest) {
   const int lane = threadIdx.x & 31;
@@ -43,7 +62,7 @@ __global__ void chain_select_kernel(const double* __restrict__ obj, const uint32
   int bj = -1;
   for (int j = lane; j < M; j += 32) {
     const int64_t k = static_cast<int64_t>(p) * M + j;
-    const double v = (flags[k] & mask) == 0u ? obj[k] : INFINITY;
+    const double v = score(obj[k], flags[k], mask, peak + k * D, budget, D);
     if (v < bv) bv = v, bj = j;  // ascending j per lane: strict < keeps the first
   }
 #pragma unroll
@@ -137,14 +156,17 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
   DevBuf<uint32_t> cubes;
   DevBuf<double> obj;
   DevBuf<uint32_t> flags;
+  DevBuf<int64_t> peak;
   cubes.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * words);
   obj.alloc(std::max<int64_t>(1, n));
   flags.alloc(std::max<int64_t>(1, n));
+  if (chains > 0) peak.alloc(static_cast<size_t>(std::max<int64_t>(1, n)) * h.D);
   std::vector<double> pool_obj;  // the population: best distinct objectives
   DevBuf<uint32_t> pool;
   pool.alloc(static_cast<size_t>(std::max(1, chains)) * words);
   std::vector<double> ho;
   std::vector<uint32_t> hf;
+  std::vector<int64_t> hp;
   auto candidates = [&](int64_t lo, int64_t cnt, uint32_t* out) {
     check_rc(xe_round_cubes(pr, so.use_lp ? x.p : nullptr, so.seed, lo, cnt, so.edits, 0.0, out, s));
     if (canonical) check_rc(xe_move_cubes(pr, out, cnt, 0, 0, cnt, 0, out, s));
@@ -152,7 +174,7 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
   for (int r = 0; r < so.rounds && n > 0; ++r) {
     const int64_t lo = so.first + (static_cast<int64_t>(r) * so.world + so.rank) * n;
     candidates(lo, n, cubes.p);
-    xe_eval_out eo{obj.p, nullptr, flags.p};
+    xe_eval_out eo{obj.p, chains > 0 ? peak.p : nullptr, flags.p};
     xe_best b{};
     check_rc(xe_eval_cubes(pr, &mo, cubes.p, n, &eo, mask, &b, s));
     res->n_valid += b.n_valid;
@@ -161,17 +183,22 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
       res->rounding_objective = b.obj;
       res->index = lo + b.index;
     }
-    if (chains <= 0 || b.n_valid == 0) continue;
-    // merge the batch's best distinct objectives into the population
+    if (chains <= 0) continue;
+    // merge the batch's best distinct scores into the population
     ho.resize(static_cast<size_t>(n));
     hf.resize(static_cast<size_t>(n));
+    hp.resize(static_cast<size_t>(n) * h.D);
     XE_CUDA(cudaMemcpyAsync(ho.data(), obj.p, n * 8, cudaMemcpyDeviceToHost, s));
     XE_CUDA(cudaMemcpyAsync(hf.data(), flags.p, n * 4, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaMemcpyAsync(hp.data(), peak.p, n * h.D * 8, cudaMemcpyDeviceToHost, s));
     XE_CUDA(cudaStreamSynchronize(s));
     std::vector<Cand> c;
     for (int i = 0; i < static_cast<int>(pool_obj.size()); ++i) c.push_back({pool_obj[static_cast<size_t>(i)], -1 - i});
-    for (int64_t i = 0; i < n; ++i)
-      if ((hf[static_cast<size_t>(i)] & mask) == 0u) c.push_back({ho[static_cast<size_t>(i)], i});
+    for (int64_t i = 0; i < n; ++i) {
+      const size_t q = static_cast<size_t>(i);
+      const double v = score(ho[q], hf[q], mask, hp.data() + q * h.D, h.budget.data(), h.D);
+      if (v < INFINITY) c.push_back({v, i});
+    }
     // pool entries first among equal objectives (they are older, lower index)
     std::stable_sort(c.begin(), c.end(), [](const Cand& a, const Cand& b) { return a.obj < b.obj; });
     DevBuf<uint32_t> next;
@@ -188,11 +215,13 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     pool = std::move(next);
     pool_obj = std::move(next_obj);
   }
-  if (res->index < 0) return;
-  res->objective = res->rounding_objective;
   DevBuf<uint32_t> inc;
   inc.alloc(words);
-  candidates(res->index, 1, inc.p);
+  bool have = res->index >= 0;
+  if (have) {
+    res->objective = res->rounding_objective;
+    candidates(res->index, 1, inc.p);
+  }
 
   // ---- local-search population
   if (chains > 0 && !pool_obj.empty()) {
@@ -202,6 +231,7 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     DevBuf<double> cur, vbest, nobj;
     DevBuf<int32_t> jbest, stalled;
     DevBuf<uint32_t> nflags;
+    DevBuf<int64_t> npeak;
     bases.alloc(static_cast<size_t>(P) * words);
     std::vector<double> cur_h(static_cast<size_t>(P));
     for (int p = 0; p < P; ++p) {
@@ -217,15 +247,17 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     nb.alloc(static_cast<size_t>(PM) * words);
     nobj.alloc(PM);
     nflags.alloc(PM);
+    npeak.alloc(static_cast<size_t>(PM) * h.D);
     double gbest = *std::min_element(cur_h.begin(), cur_h.end());
     DevBuf<uint32_t> gcube;
     gcube.alloc(words);
     const uint64_t ls_seed = (so.seed * 1000003ull + static_cast<uint64_t>(so.rank)) & 0xFFFFFFFFFFFFull;
     for (int it = 0; it < so.chain_iters; ++it) {
       check_rc(xe_move_cubes(pr, bases.p, P, ls_seed, static_cast<int64_t>(it) * PM, PM, so.max_moves, nb.p, s));
-      xe_eval_out eo{nobj.p, nullptr, nflags.p};
+      xe_eval_out eo{nobj.p, npeak.p, nflags.p};
       check_rc(xe_eval_cubes(pr, &mo, nb.p, PM, &eo, mask, nullptr, s));
-      chain_select_kernel<<<(P * 32 + 255) / 256, 256, 0, s>>>(nobj.p, nflags.p, mask, P, M, vbest.p, jbest.p);
+      chain_select_kernel<<<(P * 32 + 255) / 256, 256, 0, s>>>(nobj.p, nflags.p, npeak.p, pr->d_budget.p, h.D, mask,
+                                                                P, M, vbest.p, jbest.p);
       chain_accept_kernel<<<P, 256, 0, s>>>(nb.p, vbest.p, jbest.p, M, words, so.stall, bases.p, cur.p, stalled.p);
       XE_CUDA(cudaGetLastError());
       XE_CUDA(cudaMemcpyAsync(cur_h.data(), cur.p, P * 8, cudaMemcpyDeviceToHost, s));
@@ -239,11 +271,13 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
         res->improvements += 1;
       }
     }
-    if (gbest < res->objective) {
+    if (gbest < kOverBudget && gbest < res->objective) {
       res->objective = gbest;
       XE_CUDA(cudaMemcpyAsync(inc.p, gcube.p, words * 4, cudaMemcpyDeviceToDevice, s));
+      have = true;
     }
   }
+  if (!have) return;  // no valid schedule: objective stays inf
 
   // ---- the incumbent re-scored alone: objective bits and peaks
   DevBuf<double> o1;

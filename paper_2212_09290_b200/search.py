@@ -31,6 +31,7 @@ adds the multi-GPU exchange.
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 from typing import Optional
 
@@ -47,7 +48,8 @@ DEFAULT_MASK = _lib.F_CHECK_MASK | _lib.F_BUDGET | _lib.F_DECODE
 @dataclass
 class SearchResult:
     objective: float            # best valid objective (inf if none)
-    index: int                  # global index of the best rounding candidate (-1 if none)
+    index: int                  # global index of the best rounding candidate (-1 if none; the local
+                                # search can still find a schedule from over-budget candidates)
     cube: Optional[np.ndarray]  # the final incumbent's canonical (R, S) cube, uint32 words
     peaks: Optional[np.ndarray]  # per-device peak bytes of the incumbent
     lp_bound: Optional[float]   # PDHG LP relaxation value (lower bound), None without LP
@@ -97,7 +99,7 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
         import torch.distributed as dist
         from .shard import exchange_best, NONE
         inc = exchange_best(res.rounding_objective, res.index, res.n_valid, offset=0, device="cuda")
-        win = exchange_best(res.objective, rank if res.index >= 0 else -1, 0, offset=0, device="cuda")
+        win = exchange_best(res.objective, rank if math.isfinite(res.objective) else -1, 0, offset=0, device="cuda")
         owner = torch.tensor([rank if (res.index >= 0 and res.index == inc.index) else NONE],
                              dtype=torch.int64, device="cuda")
         dist.all_reduce(owner, op=dist.ReduceOp.MIN)
@@ -105,17 +107,17 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         n_eval, impr = int(tot[0].item()), int(tot[1].item())
         rounding, index, n_valid = inc.obj, inc.index, inc.n_valid
-        if inc.index < 0:
+        if inc.index < 0 and win.index < 0:
             obj = float("inf")
         else:
-            src = win.index if win.obj < inc.obj else int(owner.item())
+            src = win.index if (inc.index < 0 or win.obj < inc.obj) else int(owner.item())
             obj = min(win.obj, inc.obj)
             buf = torch.from_numpy(np.concatenate([cube.view(np.int32), peaks.view(np.int32)])).cuda()
             dist.broadcast(buf, src=src)
             h = buf.cpu().numpy()
             cube = h[:problem.cube_words].copy().view(np.uint32)
             peaks = h[problem.cube_words:].copy().view(np.int64)
-    has = index >= 0
+    has = math.isfinite(obj)
     return SearchResult(obj, index, cube if has else None, peaks if has else None,
                         res.lp_bound if res.has_lp else None, bool(res.lp_certified), n_eval, n_valid, impr,
                         rounding)
