@@ -4,7 +4,8 @@ config 1 (the reference's own pins, proj/tests/test_solver.cpp):
   F1 chain3 9.0 (:66-86), 8 MiB -> 9.0, 3 MiB infeasible (:88-97),
   F2 fig2 11.0 (:99-119),
   F3 chain_lowmem sweep 24, 24, 24, 24, 27 at 100/65/50/35/25 % and
-  10 MiB -> 24, 9/8 MiB -> 27, 4 MiB - 1 infeasible (:121-153);
+  10 MiB -> 24, 9/8 MiB -> 27, 4 MiB - 1 infeasible (:121-153),
+  energy: a gpu cap forces B onto the cpu -> 17.0, alpha 1 -> 18.0 (:223-249);
 and config 2 (VGG-16, strict_free): the reference's MILP optimum
 128.32908933333337 with peaks cpu 26,894,336 / gpu 60,411,904 B (HiGHS via
 solve_external)."""
@@ -125,3 +126,35 @@ def test_random_small_problems_match_reference_solve_exact():
             b = p.arrays()["budget_bytes"]
             assert (r.peaks <= b).all()
     assert not miss, miss[:5]
+
+
+def _doc(name):
+    import json
+    return json.loads(golden_problem_text(name))
+
+
+def test_energy_cap_forces_b_onto_the_cpu():
+    # test_solver.cpp:223-237: q_gpu[B] = 10 > cap 5 -> 17.0 with B on the cpu;
+    # without the cap, alpha 0 keeps the 11.0 plan
+    import json
+    from cubegen import unpack
+    doc = _doc("fig2_energy")
+    p = xe.Problem.from_json(json.dumps(doc))
+    r = search(p, xe.ModelOptions(energy=True), n_per_round=1 << 16, rounds=2)
+    assert r.objective == 17.0, r.objective
+    R, _ = unpack(r.cube[None], p.D, p.T)
+    assert R[0, 0, 2, 2] and not R[0, 1, 2, 2]
+    doc["energy"].pop("device_limit")
+    p2 = xe.Problem.from_json(json.dumps(doc))
+    assert search(p2, xe.ModelOptions(energy=True), n_per_round=1 << 16, rounds=2).objective == 11.0
+
+
+def test_energy_alpha_joins_the_objective():
+    # test_solver.cpp:239-249: chain3, alpha 1, q mirroring the compute costs -> 18.0
+    import json
+    doc = _doc("chain3")
+    dev = doc["devices"][0]["id"]
+    doc["energy"] = {"alpha": 1.0, "q_joules": {dev: [2.0, 3.0, 4.0]}, "board_joules": 0.0}
+    p = xe.Problem.from_json(json.dumps(doc))
+    r = search(p, xe.ModelOptions(energy=True), n_per_round=1 << 14, rounds=2)
+    assert r.objective == 18.0, r.objective
