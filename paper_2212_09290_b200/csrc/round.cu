@@ -91,9 +91,29 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int D = a.D, T = a.T, W = a.W32;
   const int words = 2 * D * T * W;
-  uint32_t* cube = reinterpret_cast<uint32_t*>(smem) + wid * (words + 4 * T + 4);
+  // block tables: consumers of every op as bit rows, last consumer of every op
+  uint32_t* cons = reinterpret_cast<uint32_t*>(smem);
+  int* last = reinterpret_cast<int*>(cons + T * W);
+  uint32_t* cube = reinterpret_cast<uint32_t*>(last + T) + wid * (words + T);
   int* dev = reinterpret_cast<int*>(cube + words);
-  int* last = dev + T;
+  for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
+    atomicOr(&cons[a.src[e] * W + (a.dst[e] >> 5)], 1u << (a.dst[e] & 31));
+    atomicMax(&last[a.src[e]], a.dst[e]);
+  }
+  __syncthreads();
+  // some consumer of u computed at step tt (any device)
+  auto consumer_at = [&](int u, int tt) {
+    uint32_t hit = 0u;
+    for (int w = 0; w < W; ++w) {
+      uint32_t r = 0u;
+      for (int d = 0; d < D; ++d) r |= cube[(d * T + tt) * W + w];
+      hit |= r & cons[u * W + w];
+    }
+    return hit != 0u;
+  };
   auto bit_set = [&](int which, int d, int t, int i) {
     atomicOr(&cube[((which * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
   };
@@ -108,10 +128,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
        k += static_cast<int64_t>(gridDim.x) * kRoundWarps) {
     const uint64_t c = static_cast<uint64_t>(a.first + k);
     for (int i = lane; i < words; i += 32) cube[i] = a.base ? a.base[i] : 0u;
-    // last consumer of every op (edge order independent)
-    for (int i = lane; i < T; i += 32) last[i] = -1;
     __syncwarp();
-    for (int e = lane; e < a.E; e += 32) atomicMax(&last[a.src[e]], a.dst[e]);
     if (a.base) {
       // local search around a base schedule: devices from its diagonal, then
       // (probability 1/2) one op moved with its saves to another device, then
@@ -203,25 +220,36 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
           int pickn = rng.below(n_el);
           for (i = 0; i < T; ++i)
             if (last[i] > i + 1 && pickn-- == 0) break;
-          // consumer t > i+1 of i, uniformly among its consumers
+          // consumer t > i+1 of i, uniformly among its consumers (ascending)
           int n_c = 0;
-          for (int e = 0; e < a.E; ++e) n_c += (a.src[e] == i && a.dst[e] > i + 1);
+          for (int w = 0; w < W; ++w) {
+            const int lo = w * 32;
+            uint32_t m = cons[i * W + w];
+            if (lo + 32 <= i + 2) m = 0u;
+            else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
+            n_c += __popc(m);
+          }
           int pc = rng.below(n_c);
-          for (int e = 0; e < a.E; ++e)
-            if (a.src[e] == i && a.dst[e] > i + 1 && pc-- == 0) t = a.dst[e];
+          for (int w = 0; w < W && t < 0; ++w) {
+            const int lo = w * 32;
+            uint32_t m = cons[i * W + w];
+            if (lo + 32 <= i + 2) m = 0u;
+            else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
+            const int pcnt = __popc(m);
+            if (pc < pcnt) {
+              for (int q = 0; q < pc; ++q) m &= m - 1;
+              t = lo + __ffs(m) - 1;
+            }
+            pc -= pcnt;
+          }
         }
         // the drop window must not cover a timestep where i is needed: any
         // earlier computation (diagonal or recomputed) of a consumer of i
         int a0 = i + 1;
-        for (int tt = t - 1; tt > i && a0 == i + 1; --tt)
-          for (int e = 0; e < a.E; ++e) {
-            if (a.src[e] != i) continue;
-            bool used = false;
-            for (int d = 0; d < D; ++d) used |= bit_get(0, d, tt, a.dst[e]);
-            if (used) {
-              a0 = tt + 1;
-              break;
-            }
+        for (int tt = t - 1; tt > i; --tt)
+          if (consumer_at(i, tt)) {
+            a0 = tt + 1;
+            break;
           }
         if (a0 > t) continue;
         // drop the whole window when the LP chose the spot, else a random tail of it
@@ -266,15 +294,10 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
             if (sp < 32 && a.cost[dr * T + p] < 1.0e9 && rng.uniform() < 0.5) {
               // first step after p's last use before t
               int from = p + 1;
-              for (int tt = t - 1; tt > p && from == p + 1; --tt)
-                for (int e = 0; e < a.E; ++e) {
-                  if (a.src[e] != p) continue;
-                  bool used = false;
-                  for (int d = 0; d < D; ++d) used |= bit_get(0, d, tt, a.dst[e]);
-                  if (used) {
-                    from = tt + 1;
-                    break;
-                  }
+              for (int tt = t - 1; tt > p; --tt)
+                if (consumer_at(p, tt)) {
+                  from = tt + 1;
+                  break;
                 }
               recompute_at(p, from, dr);
               stack[sp] = p;
@@ -580,7 +603,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.perturb = perturb;
   a.out = out;
   const int words = 2 * h.D * h.T * a.W32;
-  const int smem = kRoundWarps * (words + 4 * h.T + 4) * 4;
+  const int smem = (h.T * a.W32 + h.T + kRoundWarps * (words + h.T)) * 4;
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
   if (smem > limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the rounding kernel");
