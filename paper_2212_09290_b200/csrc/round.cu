@@ -409,73 +409,99 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
     const uint32_t* bc = a.base + static_cast<size_t>(k / a.per_base) * words;
     for (int i = lane; i < words; i += 32) cube[i] = i < D * T * W ? bc[i] : 0u;
     __syncwarp();
-    if (lane == 0 && a.max_moves > 0) {
+    // moves: every lane steps through them together; Philox draws stay on
+    // lane 0 (in the serial order) and are broadcast, and the R-bit counts
+    // of drop/move picks are split over the lanes (a block of rows each, an
+    // exclusive scan, the owning lane resolves the bit)
+    if (a.max_moves > 0) {
       Philox rng(a.seed, c, 0x3u);
-      const int nm = 1 + rng.below(a.max_moves);
+      const int nm = __shfl_sync(0xffffffffu, lane == 0 ? 1 + rng.below(a.max_moves) : 0, 0);
+      const int nrows = D * T, blk = (nrows + 31) / 32;
       for (int m = 0; m < nm; ++m) {
-        const double u = rng.uniform();
-        if (u < 0.4) {  // A: recompute a parent where its consumer is computed
-          const int e = rng.below(a.E);
-          const int pu = a.src[e], v = a.dst[e];
-          int cnt = 0;
-          for (int d = 0; d < D; ++d)
-            for (int t = v; t < T; ++t) cnt += rget(d, t, v);
-          if (!cnt) continue;
-          int pick = rng.below(cnt), dv = 0, tv = 0;
-          for (int d = 0; d < D && pick >= 0; ++d)
-            for (int t = v; t < T && pick >= 0; ++t)
-              if (rget(d, t, v) && pick-- == 0) dv = d, tv = t;
-          int dr = dv;
-          if (D > 1 && rng.uniform() < 0.5) dr = (dv + 1 + rng.below(D - 1)) % D;
-          if (a.cost[dr * T + pu] >= 1.0e9) dr = dv;
-          if (a.cost[dr * T + pu] >= 1.0e9) continue;
-          rw(dr, tv, pu) |= 1u << (pu & 31);
-          if (rng.uniform() < 0.5) {
-            int stack[32], sdev[32], sp = 0;
-            stack[sp] = pu;
-            sdev[sp++] = dr;
-            while (sp > 0) {
-              --sp;
-              const int x = stack[sp], dx = sdev[sp];
-              for (int q = a.in_ptr[x]; q < a.in_ptr[x + 1]; ++q) {
-                const int pp = a.src[a.in_edge[q]];
-                if (rng.uniform() >= 0.5) continue;
-                int dp = dx;
-                if (D > 1 && rng.uniform() < 0.25) dp = (dx + 1 + rng.below(D - 1)) % D;
-                if (a.cost[dp * T + pp] >= 1.0e9) dp = dx;
-                if (a.cost[dp * T + pp] >= 1.0e9 || rget(dp, tv, pp)) continue;
-                rw(dp, tv, pp) |= 1u << (pp & 31);
-                if (sp < 32) {
-                  stack[sp] = pp;
-                  sdev[sp++] = dp;
+        const double u = __shfl_sync(0xffffffffu, lane == 0 ? rng.uniform() : 0.0, 0);
+        if (u < 0.4) {  // A: recompute a parent where its consumer is computed (lane 0)
+          if (lane == 0) do {
+              const int e = rng.below(a.E);
+              const int pu = a.src[e], v = a.dst[e];
+              int cnt = 0;
+              for (int d = 0; d < D; ++d)
+                for (int t = v; t < T; ++t) cnt += rget(d, t, v);
+              if (!cnt) continue;
+              int pick = rng.below(cnt), dv = 0, tv = 0;
+              for (int d = 0; d < D && pick >= 0; ++d)
+                for (int t = v; t < T && pick >= 0; ++t)
+                  if (rget(d, t, v) && pick-- == 0) dv = d, tv = t;
+              int dr = dv;
+              if (D > 1 && rng.uniform() < 0.5) dr = (dv + 1 + rng.below(D - 1)) % D;
+              if (a.cost[dr * T + pu] >= 1.0e9) dr = dv;
+              if (a.cost[dr * T + pu] >= 1.0e9) continue;
+              rw(dr, tv, pu) |= 1u << (pu & 31);
+              if (rng.uniform() < 0.5) {
+                int stack[32], sdev[32], sp = 0;
+                stack[sp] = pu;
+                sdev[sp++] = dr;
+                while (sp > 0) {
+                  --sp;
+                  const int x = stack[sp], dx = sdev[sp];
+                  for (int q = a.in_ptr[x]; q < a.in_ptr[x + 1]; ++q) {
+                    const int pp = a.src[a.in_edge[q]];
+                    if (rng.uniform() >= 0.5) continue;
+                    int dp = dx;
+                    if (D > 1 && rng.uniform() < 0.25) dp = (dx + 1 + rng.below(D - 1)) % D;
+                    if (a.cost[dp * T + pp] >= 1.0e9) dp = dx;
+                    if (a.cost[dp * T + pp] >= 1.0e9 || rget(dp, tv, pp)) continue;
+                    rw(dp, tv, pp) |= 1u << (pp & 31);
+                    if (sp < 32) {
+                      stack[sp] = pp;
+                      sdev[sp++] = dp;
+                    }
+                  }
                 }
               }
+          } while (false);
+          __syncwarp();
+          continue;
+        }
+        // B / C: pick an R bit (B: off the diagonal)
+        const bool drop = u < 0.65;
+        auto row_bits = [&](int r, int w) {
+          const int t = r % T;
+          uint32_t x = cube[r * W + w];
+          if (drop && (t >> 5) == w) x &= ~(1u << (t & 31));
+          return x;
+        };
+        int mine = 0;
+        for (int r = lane * blk; r < min(nrows, (lane + 1) * blk); ++r)
+          for (int w = 0; w < W; ++w) mine += __popc(row_bits(r, w));
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int cnt = __shfl_sync(0xffffffffu, incl, 31);
+        if (!cnt) continue;
+        const int pick = __shfl_sync(0xffffffffu, lane == 0 ? rng.below(cnt) : 0, 0);
+        const int excl = incl - mine;
+        int code = -1;  // (r * W + w) * 32 + bit
+        if (pick >= excl && pick < incl) {
+          int rem = pick - excl;
+          for (int r = lane * blk; r < min(nrows, (lane + 1) * blk) && code < 0; ++r)
+            for (int w = 0; w < W && code < 0; ++w) {
+              uint32_t x = row_bits(r, w);
+              const int pc = __popc(x);
+              if (rem < pc) {
+                for (int q = 0; q < rem; ++q) x &= x - 1;
+                code = (r * W + w) * 32 + __ffs(x) - 1;
+              }
+              rem -= pc;
             }
-          }
-        } else {  // B / C: pick an R bit (B: off the diagonal)
-          const bool drop = u < 0.65;
-          int cnt = 0;
-          for (int d = 0; d < D; ++d)
-            for (int t = 0; t < T; ++t)
-              for (int w = 0; w < W; ++w) {
-                uint32_t x = rw(d, t, w * 32);
-                if (drop && (t >> 5) == w) x &= ~(1u << (t & 31));
-                cnt += __popc(x);
-              }
-          if (!cnt) continue;
-          int pick = rng.below(cnt), pd = 0, pt = 0, pi = 0;
-          for (int d = 0; d < D && pick >= 0; ++d)
-            for (int t = 0; t < T && pick >= 0; ++t)
-              for (int w = 0; w < W && pick >= 0; ++w) {
-                uint32_t x = rw(d, t, w * 32);
-                if (drop && (t >> 5) == w) x &= ~(1u << (t & 31));
-                const int pc = __popc(x);
-                if (pick < pc) {
-                  for (int q = 0; q < pick; ++q) x &= x - 1;
-                  pd = d, pt = t, pi = w * 32 + __ffs(x) - 1;
-                }
-                pick -= pc;
-              }
+        }
+        const unsigned own = __ballot_sync(0xffffffffu, code >= 0);
+        code = __shfl_sync(0xffffffffu, code, __ffs(own) - 1);
+        if (lane == 0) {
+          const int r = code / 32 / W, w = (code / 32) % W;
+          const int pd = r / T, pt = r % T, pi = w * 32 + (code & 31);
           rw(pd, pt, pi) &= ~(1u << (pi & 31));
           if (!drop) {
             int to = pd;
@@ -484,6 +510,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
             rw(to, pt, pi) |= 1u << (pi & 31);
           }
         }
+        __syncwarp();
       }
     }
     __syncwarp();
