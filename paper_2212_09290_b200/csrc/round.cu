@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   // block tables: consumers of every op as bit rows, last consumer of every op
   uint32_t* cons = reinterpret_cast<uint32_t*>(smem);
   int* last = reinterpret_cast<int*>(cons + T * W);
-  uint32_t* cube = reinterpret_cast<uint32_t*>(last + T) + wid * (words + T);
+  int* elig = last + T;      // ops with a consumer beyond i+1, ascending
+  int* n_elig = elig + T;
+  uint32_t* cube = reinterpret_cast<uint32_t*>(n_elig + 1) + wid * (words + T);
   int* dev = reinterpret_cast<int*>(cube + words);
   for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
   for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
@@ -102,6 +104,13 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
     atomicOr(&cons[a.src[e] * W + (a.dst[e] >> 5)], 1u << (a.dst[e] & 31));
     atomicMax(&last[a.src[e]], a.dst[e]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ne = 0;
+    for (int j = 0; j < T; ++j)
+      if (last[j] > j + 1) elig[ne++] = j;
+    *n_elig = ne;
   }
   __syncthreads();
   // some consumer of u computed at step tt (any device)
@@ -117,8 +126,12 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   auto bit_set = [&](int which, int d, int t, int i) {
     atomicOr(&cube[((which * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
   };
-  auto bit_clr = [&](int which, int d, int t, int i) {
-    atomicAnd(&cube[((which * D + d) * T + t) * W + (i >> 5)], ~(1u << (i & 31)));
+  // plain read-modify-write for the single-lane sections (lane 0 edits)
+  auto bset = [&](int which, int d, int t, int i) {
+    cube[((which * D + d) * T + t) * W + (i >> 5)] |= 1u << (i & 31);
+  };
+  auto bclr = [&](int which, int d, int t, int i) {
+    cube[((which * D + d) * T + t) * W + (i >> 5)] &= ~(1u << (i & 31));
   };
   auto bit_get = [&](int which, int d, int t, int i) -> bool {
     return (cube[((which * D + d) * T + t) * W + (i >> 5)] >> (i & 31)) & 1u;
@@ -146,12 +159,12 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
           const int i = 1 + rng.below(T - 1), from = dev[i];
           const int to = (from + 1 + rng.below(D - 1)) % D;
           if (a.cost[to * T + i] < 1.0e9) {
-            bit_clr(0, from, i, i);
-            bit_set(0, to, i, i);
+            bclr(0, from, i, i);
+            bset(0, to, i, i);
             for (int t = i + 1; t < T; ++t)
               if (bit_get(1, from, t, i)) {
-                bit_clr(1, from, t, i);
-                bit_set(1, to, t, i);
+                bclr(1, from, t, i);
+                bset(1, to, t, i);
               }
             dev[i] = to;
           }
@@ -214,12 +227,9 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
           lp_dev = code / (T * T);
         } else {
           // op i with a consumer beyond i+1, chosen uniformly among eligible ops
-          int n_el = 0;
-          for (int j = 0; j < T; ++j) n_el += last[j] > j + 1;
+          const int n_el = *n_elig;
           if (n_el == 0) break;
-          int pickn = rng.below(n_el);
-          for (i = 0; i < T; ++i)
-            if (last[i] > i + 1 && pickn-- == 0) break;
+          i = elig[rng.below(n_el)];
           // consumer t > i+1 of i, uniformly among its consumers (ascending)
           int n_c = 0;
           for (int w = 0; w < W; ++w) {
@@ -260,13 +270,13 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
         // over [from, t]; later saves follow it to dr (EQ11 needs a holder at t)
         auto recompute_at = [&](int v, int from, int dr) {
           const int dv = dev[v];
-          for (int tt = from; tt <= t; ++tt) bit_clr(1, dv, tt, v);
-          bit_set(0, dr, t, v);
+          for (int tt = from; tt <= t; ++tt) bclr(1, dv, tt, v);
+          bset(0, dr, t, v);
           if (dr != dv)
             for (int tt = t + 1; tt < T; ++tt)
               if (bit_get(1, dv, tt, v)) {
-                bit_clr(1, dv, tt, v);
-                bit_set(1, dr, tt, v);
+                bclr(1, dv, tt, v);
+                bset(1, dr, tt, v);
               }
         };
         recompute_at(i, a1, dn);
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
             int ls = p;
             for (int tt = p + 1; tt <= t; ++tt)
               if (bit_get(1, dp, tt, p)) ls = tt;
-            for (int tt = ls + 1; tt <= t; ++tt) bit_set(1, dp, tt, p);
+            for (int tt = ls + 1; tt <= t; ++tt) bset(1, dp, tt, p);
           }
         }
       }
@@ -630,7 +640,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.perturb = perturb;
   a.out = out;
   const int words = 2 * h.D * h.T * a.W32;
-  const int smem = (h.T * a.W32 + h.T + kRoundWarps * (words + h.T)) * 4;
+  const int smem = (h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T)) * 4;
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
   if (smem > limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the rounding kernel");
