@@ -403,12 +403,16 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
   const int D = a.D, T = a.T, W = a.W32;
   const int words = 2 * D * T * W;
   uint32_t* cons = reinterpret_cast<uint32_t*>(smem);  // [T][W] consumers of u
-  uint32_t* cube = cons + T * W + wid * (words + T * W);
+  uint32_t* par = cons + T * W;                        // [T][W] parents of v
+  uint32_t* cube = par + T * W + wid * (words + 2 * T * W);
   uint32_t* rany = cube + words;  // [T][W] ops computed at t (any device)
-  for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
+  uint32_t* hbuf = rany + T * W;  // [T][W] hold(., t)
+  for (int i = threadIdx.x; i < 2 * T * W; i += blockDim.x) cons[i] = 0u;
   __syncthreads();
-  for (int e = threadIdx.x; e < a.E; e += blockDim.x)
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
     atomicOr(&cons[a.src[e] * W + (a.dst[e] >> 5)], 1u << (a.dst[e] & 31));
+    atomicOr(&par[a.dst[e] * W + (a.src[e] >> 5)], 1u << (a.src[e] & 31));
+  }
   __syncthreads();
   auto rw = [&](int d, int t, int i) -> uint32_t& { return cube[(d * T + t) * W + (i >> 5)]; };
   auto rget = [&](int d, int t, int i) -> bool { return (rw(d, t, i) >> (i & 31)) & 1u; };
@@ -524,7 +528,12 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
       }
     }
     __syncwarp();
-    // canonical saves
+    // canonical saves, bit-parallel over the ops (lane w < W owns word w):
+    //   need_t = parents of the ops computed at t, comp_t = ops computed at t
+    //   backward: H_t = ~comp_t & (need_t | H_{t+1})   (hold(u,t) = bit u of H_t:
+    //             the next need comes before the next computation)
+    //   forward:  own_d = ops whose latest computation so far ran on d (lowest
+    //             d among simultaneous ones); S(d,t) = H_t & own_d
     for (int i = lane; i < T * W; i += 32) {
       const int t = i / W, w = i % W;
       uint32_t x = 0u;
@@ -532,23 +541,27 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
       rany[i] = x;
     }
     __syncwarp();
-    for (int u = lane; u < T; u += 32) {
-      uint32_t hold[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      int nn = T, nc = T;
+    if (lane < W) {
+      const int w = lane;
+      uint32_t H = 0u;
       for (int t = T - 1; t >= 0; --t) {
-        bool need = false;
-        for (int w = 0; w < W; ++w) need |= (rany[t * W + w] & cons[u * W + w]) != 0u;
-        if ((rany[t * W + (u >> 5)] >> (u & 31)) & 1u) nc = t;
-        if (need) nn = t;
-        if (nn < nc) hold[t >> 5] |= 1u << (t & 31);
+        uint32_t need = 0u;
+        for (int ww = 0; ww < W; ++ww)
+          for (uint32_t b = rany[t * W + ww]; b; b &= b - 1) need |= par[(ww * 32 + __ffs(b) - 1) * W + w];
+        H = ~rany[t * W + w] & (need | H);
+        hbuf[t * W + w] = H;
       }
-      int hd = -1;
+      uint32_t own[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
       for (int t = 0; t < T; ++t) {
-        if ((rany[t * W + (u >> 5)] >> (u & 31)) & 1u) {
-          for (int d = D - 1; d >= 0; --d)
-            if (rget(d, t, u)) hd = d;
-        } else if (hd >= 0 && ((hold[t >> 5] >> (t & 31)) & 1u)) {
-          atomicOr(&cube[((D + hd) * T + t) * W + (u >> 5)], 1u << (u & 31));
+        const uint32_t Ht = hbuf[t * W + w], comp = rany[t * W + w];
+        uint32_t taken = 0u;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          if (d >= D) break;
+          cube[((D + d) * T + t) * W + w] = Ht & own[d];
+          const uint32_t r = cube[(d * T + t) * W + w] & ~taken;
+          own[d] = (own[d] & ~comp) | r;
+          taken |= r;
         }
       }
     }
@@ -660,7 +673,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
 // ops-computed-at-t rows
 int move_smem_bytes(const HostProblem& h) {
   const int W = (h.T + 31) / 32, words = 2 * h.D * h.T * W;
-  return (h.T * W + kRoundWarps * (words + h.T * W)) * 4;
+  return (2 * h.T * W + kRoundWarps * (words + 2 * h.T * W)) * 4;
 }
 
 bool move_supported(const xe_problem* pr) {
