@@ -5,7 +5,6 @@
 import json
 import os
 
-import numpy as np
 import pytest
 
 from conftest import GOLDEN, golden_problem_text

@@ -9,7 +9,6 @@ config 1 (the reference's own pins, proj/tests/test_solver.cpp):
 and config 2 (VGG-16, strict_free): the reference's MILP optimum
 128.32908933333337 with peaks cpu 26,894,336 / gpu 60,411,904 B (HiGHS via
 solve_external)."""
-import numpy as np
 import pytest
 
 from conftest import golden_problem_text
