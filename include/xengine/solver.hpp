@@ -50,6 +50,7 @@ struct SearchParams {
   int chain_iters = 100;
   int max_moves = 4;
   int stall = 15;
+  SearchLimits limits;      // time_limit_ms honoured (node_limit: candidates are not nodes)
 };
 
 // Best schedule by the GPU search: K1 model -> K3 LP relaxation -> K4

@@ -357,6 +357,9 @@ typedef struct xe_search_opts {
   int32_t stall;         /* iterations without improvement before a kick (15) */
   int64_t first;         /* global index of the first rounded candidate (0) */
   int32_t rank, world;   /* candidate sharding (0, 1) */
+  int64_t time_limit_ms; /* wall-clock limit (0 = none): later rounding rounds and
+                            local-search iterations are skipped once it is spent
+                            (SearchLimits::time_limit_ms, solver.hpp:22-25) */
 } xe_search_opts;
 
 typedef struct xe_search_result {
@@ -368,7 +371,7 @@ typedef struct xe_search_result {
   int32_t has_lp, lp_certified;
   int64_t n_evaluated, n_valid; /* candidates scored; valid rounding candidates */
   int32_t improvements;       /* local-search improvements of the incumbent */
-  int32_t reserved;
+  int32_t time_limited;       /* 1: the time limit cut the search short */
 } xe_search_result;
 
 void xe_search_opts_default(xe_search_opts* o);

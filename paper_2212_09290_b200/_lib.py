@@ -117,14 +117,15 @@ class SearchOpts(C.Structure):
                 ("seed", C.c_uint64), ("use_lp", C.c_int32), ("lp_tol", C.c_double),
                 ("valid_mask", C.c_uint32), ("canonical", C.c_int32), ("chains", C.c_int32),
                 ("chain_n", C.c_int32), ("chain_iters", C.c_int32), ("max_moves", C.c_int32),
-                ("stall", C.c_int32), ("first", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("stall", C.c_int32), ("first", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32),
+                ("time_limit_ms", C.c_int64)]
 
 
 class SearchResult(C.Structure):
     _fields_ = [("objective", C.c_double), ("rounding_objective", C.c_double), ("index", C.c_int64),
                 ("lp_bound", C.c_double), ("has_lp", C.c_int32), ("lp_certified", C.c_int32),
                 ("n_evaluated", C.c_int64), ("n_valid", C.c_int64), ("improvements", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("time_limited", C.c_int32)]
 
 
 # symbol -> (restype, argtypes); the set of exports include/xengine_b200.h declares

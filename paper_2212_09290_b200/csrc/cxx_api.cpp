@@ -923,6 +923,7 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
   so.chain_iters = params.chain_iters;
   so.max_moves = params.max_moves;
   so.stall = params.stall;
+  so.time_limit_ms = params.limits.time_limit_ms.value_or(0);
   const xe_model_opts o = c_opts(opts);
   xe_search_result r{};
   std::vector<uint32_t> cube(xe_cube_bytes(D, T) / 4);

@@ -27,6 +27,7 @@
 // candidates (tight budgets where the rounding finds no valid schedule)
 // first descend to feasibility; anything else is never accepted.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -117,6 +118,12 @@ struct Cand {
 void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_search_opts& so, xe_search_result* res,
                    uint32_t* cube_host, int64_t* peaks_host, cudaStream_t s) {
   const HostProblem& h = pr->h;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto out_of_time = [&] {
+    if (so.time_limit_ms <= 0) return false;
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t_start);
+    return ms.count() >= so.time_limit_ms;
+  };
   const int words = 2 * h.D * h.T * ((h.T + 31) / 32);
   const bool movable = move_supported(pr);  // the move kernel's cube fits shared memory
   const bool canonical = so.canonical && movable;
@@ -172,6 +179,10 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     if (canonical) check_rc(xe_move_cubes(pr, out, cnt, 0, 0, cnt, 0, out, s));
   };
   for (int r = 0; r < so.rounds && n > 0; ++r) {
+    if (r > 0 && out_of_time()) {
+      res->time_limited = 1;
+      break;
+    }
     const int64_t lo = so.first + (static_cast<int64_t>(r) * so.world + so.rank) * n;
     candidates(lo, n, cubes.p);
     xe_eval_out eo{obj.p, chains > 0 ? peak.p : nullptr, flags.p};
@@ -253,6 +264,10 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     gcube.alloc(words);
     const uint64_t ls_seed = (so.seed * 1000003ull + static_cast<uint64_t>(so.rank)) & 0xFFFFFFFFFFFFull;
     for (int it = 0; it < so.chain_iters; ++it) {
+      if (out_of_time()) {
+        res->time_limited = 1;
+        break;
+      }
       check_rc(xe_move_cubes(pr, bases.p, P, ls_seed, static_cast<int64_t>(it) * PM, PM, so.max_moves, nb.p, s));
       xe_eval_out eo{nobj.p, npeak.p, nflags.p};
       check_rc(xe_eval_cubes(pr, &mo, nb.p, PM, &eo, mask, nullptr, s));
@@ -316,6 +331,7 @@ extern "C" void xe_search_opts_default(xe_search_opts* o) {
   o->first = 0;
   o->rank = 0;
   o->world = 1;
+  o->time_limit_ms = 0;
 }
 
 extern "C" int xe_search(const xe_problem* p, const xe_model_opts* opts, const xe_search_opts* so,

@@ -58,13 +58,15 @@ class SearchResult:
     n_valid: int                # valid rounding candidates
     ls_improvements: int = 0    # improvements of the incumbent found by the local search
     rounding_objective: float = float("inf")  # best rounding candidate alone
+    time_limited: bool = False  # time_limit_ms cut the search short (on some rank)
 
 
 def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: int = 1 << 18,
            rounds: int = 4, seed: int = 1, edits: int = 3, use_lp: bool = True,
            valid_mask: int = DEFAULT_MASK, first: int = 0, lp_tol: float = 1e-6,
            distributed: bool = False, chains: int = 256, chain_n: int = 1024, chain_iters: int = 100,
-           max_moves: int = 4, stall: int = 15, canonical: bool = True) -> SearchResult:
+           max_moves: int = 4, stall: int = 15, canonical: bool = True,
+           time_limit_ms: int = 0) -> SearchResult:
     """One native call (xe_search, csrc/search.cu) per GPU.
     distributed=True (torch.distributed initialised, one process per GPU):
     rank r rounds global index blocks (round * world + r) * n_per_round and
@@ -86,7 +88,7 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
     so.n_per_round, so.rounds, so.edits, so.seed = n_per_round, rounds, edits, seed
     so.use_lp, so.lp_tol, so.valid_mask, so.canonical = int(use_lp), lp_tol, valid_mask, int(canonical)
     so.chains, so.chain_n, so.chain_iters, so.max_moves, so.stall = chains, chain_n, chain_iters, max_moves, stall
-    so.first, so.rank, so.world = first, rank, world
+    so.first, so.rank, so.world, so.time_limit_ms = first, rank, world, time_limit_ms
     res = _lib.SearchResult()
     cube = np.zeros(problem.cube_words, np.uint32)
     peaks = np.zeros(problem.D, np.int64)
@@ -118,6 +120,11 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
             cube = h[:problem.cube_words].copy().view(np.uint32)
             peaks = h[problem.cube_words:].copy().view(np.int64)
     has = math.isfinite(obj)
+    limited = bool(res.time_limited)
+    if world > 1:
+        t = torch.tensor([int(limited)], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        limited = bool(t.item())
     return SearchResult(obj, index, cube if has else None, peaks if has else None,
                         res.lp_bound if res.has_lp else None, bool(res.lp_certified), n_eval, n_valid, impr,
-                        rounding)
+                        rounding, limited)

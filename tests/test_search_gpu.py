@@ -168,3 +168,14 @@ def test_vgg16_default_hazard_decodable_optimum():
     r = search(p, xe.ModelOptions(strict_free=False), n_per_round=1 << 20, rounds=2, edits=6, seed=1)
     assert r.objective == VGG_OPT, r.objective
     assert (r.peaks <= p.arrays()["budget_bytes"]).all()
+
+
+def test_time_limit_cuts_the_local_search():
+    import time
+    from bench import configs
+    p = xe.Problem.from_json(configs.vgg16_doc())
+    t0 = time.time()
+    r = search(p, xe.ModelOptions(strict_free=True), n_per_round=1 << 18, rounds=1, chain_iters=1_000_000,
+               time_limit_ms=1500)
+    assert r.time_limited and time.time() - t0 < 20
+    assert r.objective < float("inf") and r.objective <= r.rounding_objective
