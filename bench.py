@@ -167,6 +167,17 @@ def resnet_pipeline(args):
                      "roofline": {"bound": "hbm", "bytes_per_iter": it_bytes,
                                   "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}},
             "clocks": clk.summary(), "gpu_launches": 2 * args.steps}
+    if not args.skip_search:
+        from paper_2212_09290_b200.search import search
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sr = search(prob, n_per_round=1 << 16, rounds=4, edits=6, seed=1, chain_n=256)
+        torch.cuda.synchronize()
+        line["search"] = {"workload": "resnet50 cfg3 best schedule: K1 -> K3 LP -> K4 rounding + R-space local search -> K2",
+                          "objective": sr.objective, "rounding_objective": sr.rounding_objective,
+                          "lp_bound": sr.lp_bound, "gap_to_lp": sr.objective / sr.lp_bound - 1.0,
+                          "candidates_evaluated": sr.n_evaluated, "seconds": time.perf_counter() - t0,
+                          "reference": "no optimum (solve_exact needs D*T <= 64; HiGHS cannot solve the MILP)"}
     print(json.dumps(line), flush=True)
 
 
