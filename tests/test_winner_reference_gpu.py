@@ -17,6 +17,8 @@ torch = pytest.importorskip("torch")
 import paper_2212_09290_b200 as xe  # noqa: E402
 from paper_2212_09290_b200.search import DEFAULT_MASK, search  # noqa: E402
 
+_MASK = DEFAULT_MASK
+
 
 @pytest.fixture(scope="module")
 def ref():
@@ -57,3 +59,33 @@ def test_search_winner_and_top_candidates_rescored_by_reference(ref, name):
     # the GPU winner of the batch is the reference's winner among the re-scored
     w = pick[np.argmin(np.where(ref_flags_valid(rf), ro, np.inf))]
     assert w == res.best_index
+
+
+def test_vgg16_bench_scale_batch_rescored_by_reference(ref):
+    """The bench's workload shape (config 2, K4 candidates with 10 % bit
+    flips, interleaved layout) at 2 M candidates: the batch winner and a
+    deterministic sample of 64, re-scored by the reference library."""
+    text = configs.vgg16_doc()
+    prob = xe.Problem.from_json(text)
+    rp = ref.load(text)
+    n = 2_000_000
+    cubes = xe.round_cubes(prob, n, seed=2212, edits=3, perturb=0.1)
+    il = xe.cubes_to_il(prob, cubes)
+    res = xe.evaluate_cubes_il(prob, il, n, valid_mask=_MASK)
+    pick = np.unique(np.concatenate([np.random.default_rng(5).choice(n, 64, replace=False), [res.best_index]]))
+    host = cubes[torch.from_numpy(pick).cuda()].cpu().numpy().view(np.uint32)
+    ro, rpk, rf = rp.eval_cubes(host, prob.D, nthreads=8)
+    sel = torch.from_numpy(pick).cuda()
+    assert np.array_equal(ro.view(np.int64), res.obj[sel].cpu().numpy().view(np.int64))
+    assert np.array_equal(rpk, res.peak[sel].cpu().numpy())
+    f = res.flags[sel].cpu().numpy().astype(np.uint32)
+    rf = rf.astype(np.uint32)
+    # every check_assignment family, BUDGET and DECODE bit-exact; DECODE_FREED
+    # (which decode error came first) only where no parent is missing: the
+    # reference reports its first decode error only (tests/test_eval_gpu.py)
+    mask = np.uint32(0xFFFF | xe._lib.F_DECODE)
+    assert np.array_equal(f & mask, rf & mask)
+    comparable = ((rf & xe._lib.F_DECODE) != 0) & ((f & xe._lib.F_EQ12) == 0)
+    assert np.array_equal((f & xe._lib.F_DECODE_FREED)[comparable], (rf & xe._lib.F_DECODE_FREED)[comparable])
+    w = int(np.flatnonzero(pick == res.best_index)[0])
+    assert ref_flags_valid(rf)[w] and ro[w] == res.best_obj
