@@ -247,6 +247,18 @@ def placement_sweep(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "bytes_per_candidate": bpc},
             "clocks": clk.summary(), "gpu_launches": 2 * args.steps}
+    if rank == 0 and not args.skip_search:
+        from paper_2212_09290_b200.search import search_placements
+        del dev
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sp = search_placements(prob, iters=1000)
+        torch.cuda.synchronize()
+        line["search"] = {"workload": "cfg5 best save-all placement: 4 M uniform placements, then 256 local-search "
+                                      "chains x 1024 neighbours x 1000 iterations (K2b exact scoring)",
+                          "objective": sp.objective, "random_sample_objective": sp.random_objective,
+                          "placements_evaluated": sp.n_evaluated, "seconds": time.perf_counter() - t0,
+                          "reference": "assignment_oracle stops at 4e6 placements (8^2000 here)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -128,3 +128,85 @@ def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: i
     return SearchResult(obj, index, cube if has else None, peaks if has else None,
                         res.lp_bound if res.has_lp else None, bool(res.lp_certified), n_eval, n_valid, impr,
                         rounding, limited)
+
+
+@dataclass
+class PlacementSearchResult:
+    objective: float             # best valid save-all (or minimal-save) objective, inf if none
+    dev: Optional[np.ndarray]    # its device vector [T]
+    peaks: Optional[np.ndarray]  # its per-device peaks
+    random_objective: float      # best of the random sample alone
+    n_evaluated: int
+    improvements: int
+
+
+def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 256, chain_n: int = 1024,
+                      iters: int = 100, max_moves: int = 4, stall: int = 15, seed: int = 1, policy: int = 0,
+                      valid_mask: int = _lib.F_CHECK_MASK | _lib.F_BUDGET) -> PlacementSearchResult:
+    """Best placement where the D^T sweep of assignment_oracle (solver.cpp:44-75,
+    capped at 4e6 placements) cannot go — config 5 has 8^2000: K2b scores
+    `n_random` uniform placements (xe_random_placements), the best distinct
+    valid ones seed `chains` iterated local searches whose neighbours change
+    the device of 1..max_moves random ops (to a device that can run them);
+    each iteration scores chains x chain_n neighbours exactly (K2b) and a
+    chain moves to its best valid neighbour when it improves, or after
+    `stall` iterations without improvement."""
+    import torch
+    from .api import evaluate_placements, random_placements
+    T, D = problem.T, problem.D
+    a = problem.arrays()
+    allowed = torch.from_numpy(np.asarray(a["cost_ms"]).reshape(D, T).T < 1e9).cuda()  # [T, D]
+    dev = random_placements(problem, n_random, seed)
+    r = evaluate_placements(problem, dev, policy=policy, valid_mask=valid_mask)
+    score = torch.where((r.flags & valid_mask) == 0, r.obj, torch.full_like(r.obj, float("inf")))
+    rand_best = float(score.min().item())
+    if not np.isfinite(rand_best):
+        return PlacementSearchResult(float("inf"), None, None, rand_best, n_random, 0)
+    v, i = torch.sort(score)
+    keep, last = [], None
+    for val, idx in zip(v[:16 * chains].tolist(), i[:16 * chains].tolist()):
+        if not np.isfinite(val):
+            break
+        if val != last:
+            keep.append(idx)
+            last = val
+        if len(keep) == chains:
+            break
+    sel = torch.tensor([keep[k % len(keep)] for k in range(chains)], device="cuda")
+    bases, cur = dev[sel].clone(), score[sel].clone()
+    del dev, r, score
+    P, M = chains, chain_n
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    stalled = torch.zeros(P, dtype=torch.int32, device="cuda")
+    rows = torch.arange(P, device="cuda") * M
+    best = float(cur.min().item())
+    best_dev = bases[int(torch.argmin(cur))].clone()
+    improvements, n_eval = 0, n_random
+    cols = torch.arange(max_moves, device="cuda")
+    for _ in range(iters):
+        nb = bases.repeat_interleave(M, dim=0)
+        nm = torch.randint(1, max_moves + 1, (P * M, 1), device="cuda", generator=g)
+        pos = torch.randint(0, T, (P * M, max_moves), device="cuda", generator=g)
+        new = torch.randint(0, D, (P * M, max_moves), device="cuda", generator=g, dtype=torch.int64)
+        ok = (cols[None, :] < nm) & allowed[pos, new]
+        cur_dev = torch.gather(nb, 1, pos).to(torch.int64)
+        nb.scatter_(1, pos, torch.where(ok, new, cur_dev).to(torch.uint8))
+        r = evaluate_placements(problem, nb, policy=policy, valid_mask=valid_mask, best=False)
+        n_eval += P * M
+        s = torch.where((r.flags & valid_mask) == 0, r.obj, torch.full_like(r.obj, float("inf"))).view(P, M)
+        v, j = s.min(1)
+        take = (v < cur) | ((stalled >= stall) & torch.isfinite(v))
+        bases = torch.where(take[:, None], nb[rows + j], bases)
+        stalled = torch.where(v < cur, torch.zeros_like(stalled), torch.where(take, torch.zeros_like(stalled),
+                                                                               stalled + 1))
+        cur = torch.where(take, v, cur)
+        b = float(cur.min().item())
+        if b < best:
+            best, best_dev = b, bases[int(torch.argmin(cur))].clone()
+            improvements += 1
+        del nb, r, s
+    r1 = evaluate_placements(problem, best_dev.unsqueeze(0).contiguous(), policy=policy, valid_mask=valid_mask)
+    assert r1.best_obj == best, (r1.best_obj, best)
+    return PlacementSearchResult(best, best_dev.cpu().numpy(), r1.peak.cpu().numpy()[0], rand_best, n_eval,
+                                 improvements)

@@ -179,3 +179,17 @@ def test_time_limit_cuts_the_local_search():
                time_limit_ms=1500)
     assert r.time_limited and time.time() - t0 < 20
     assert r.objective < float("inf") and r.objective <= r.rounding_objective
+
+
+def test_placement_search_fig2_and_config5():
+    # fig2: the assignment_oracle optimum 11.0 (test_solver.cpp:99-119);
+    # config 5 (8^2000 placements, beyond the oracle): the local search beats
+    # the best of the random sample, stays within budgets, re-scores exactly
+    from bench import configs
+    from paper_2212_09290_b200.search import search_placements
+    r = search_placements(prob("fig2"), n_random=1 << 10, chains=16, chain_n=64, iters=10)
+    assert r.objective == 11.0, r.objective
+    p5 = xe.Problem.from_json(configs.random2000_doc())
+    r5 = search_placements(p5, n_random=1 << 18, chains=64, chain_n=256, iters=20, seed=3)
+    assert r5.objective < r5.random_objective and r5.improvements > 0
+    assert (r5.peaks <= p5.arrays()["budget_bytes"]).all()
