@@ -325,6 +325,11 @@ int xe_mutate_cubes(const xe_problem* p, const uint32_t* base_dev, uint64_t seed
  * Candidate k is a pure function of (seed, first + k, its base).  T <= 256. */
 int xe_move_cubes(const xe_problem* p, const uint32_t* base_dev, int64_t n_base, uint64_t seed, int64_t first,
                   int64_t n, int32_t max_moves, uint32_t* cubes_dev, void* stream);
+/* Placement-space neighbours (device buffers): neighbour k copies base
+ * k / (n / n_base) ([n_base][T] u8) and moves 1..max_moves random ops to a
+ * random device that can run them; a pure function of (seed, first + k). */
+int xe_move_placements(const xe_problem* p, const uint8_t* base_dev, int64_t n_base, uint64_t seed, int64_t first,
+                       int64_t n, int32_t max_moves, uint8_t* dev_out, void* stream);
 /* n uniform random placements dev[n][T] (device buffer): op i on a device
  * that can run it (cost < 1e9), candidate k a pure function of
  * (seed, first + k) — the input family of config 5's placement sweep. */

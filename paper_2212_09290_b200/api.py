@@ -248,6 +248,22 @@ def move_cubes(problem: Problem, base, n: int, seed: int, first: int = 0, max_mo
     return out
 
 
+def move_placements(problem: Problem, base, n: int, seed: int, first: int = 0, max_moves: int = 4, out=None,
+                    stream=None):
+    """K4 placement-space neighbours: base uint8 CUDA tensor [n_base, T] (or
+    [T]); neighbour k copies base k // (n // n_base) and moves 1..max_moves
+    random ops to a random allowed device."""
+    import torch
+    b = base.unsqueeze(0) if base.dim() == 1 else base
+    b = b.contiguous()
+    if out is None:
+        out = torch.empty((n, problem.T), dtype=torch.uint8, device=b.device)
+    s = stream if stream is not None else torch.cuda.current_stream(out.device).cuda_stream
+    check(LIB.xe_move_placements(problem.handle, C.c_void_p(b.data_ptr()), b.shape[0], seed, first, n, max_moves,
+                                 C.c_void_p(out.data_ptr()), C.c_void_p(s)))
+    return out
+
+
 def random_placements(problem: Problem, n: int, seed: int, first: int = 0, out=None, stream=None):
     """n uniform random placements (uint8 CUDA tensor [n, T]); candidate k is
     a pure function of (seed, first + k)."""

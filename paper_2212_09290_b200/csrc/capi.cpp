@@ -25,6 +25,8 @@ void eval_cubes_device(const xe_problem* pr, const xe_model_opts& opts, const ui
                        uint64_t* best3, unsigned char* scratch, cudaStream_t stream);
 void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_base, uint64_t seed, int64_t first,
                        int64_t n, int max_moves, uint32_t* out, cudaStream_t s);
+void move_placements_device(const xe_problem* pr, const uint8_t* base, int64_t n_base, uint64_t seed, int64_t first,
+                            int64_t n, int max_moves, uint8_t* out, cudaStream_t s);
 void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, int64_t first,
                         int64_t n, int edits, double perturb, uint32_t* out, cudaStream_t s,
                         const uint32_t* base = nullptr);
@@ -427,6 +429,16 @@ int xe_move_cubes(const xe_problem* p, const uint32_t* base_dev, int64_t n_base,
       fail(XE_ERR_ARG, "bad argument (n must be a multiple of n_base >= 1)");
     require_uploaded(p);
     move_cubes_device(p, base_dev, n_base, seed, first, n, max_moves, cubes_dev, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int xe_move_placements(const xe_problem* p, const uint8_t* base_dev, int64_t n_base, uint64_t seed, int64_t first,
+                       int64_t n, int32_t max_moves, uint8_t* dev_out, void* stream) {
+  return guard([&] {
+    if (!p || !base_dev || (!dev_out && n > 0) || n < 0 || max_moves < 1 || n_base < 1 || n % n_base)
+      fail(XE_ERR_ARG, "bad argument (n must be a multiple of n_base >= 1, max_moves >= 1)");
+    require_uploaded(p);
+    move_placements_device(p, base_dev, n_base, seed, first, n, max_moves, dev_out, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -571,6 +571,41 @@ __global__ void __launch_bounds__(kRoundWarps * 32) move_kernel(const MoveArgs a
     __syncwarp();
   }
 }
+
+// Placement-space neighbours (config 5's local search): neighbour k copies
+// base k / per_base and moves 1..max_moves random ops to a random device
+// that can run them (a draw of a device that cannot leaves the op where it
+// is).  One warp per neighbour: 16-byte copies by all lanes, the moves by
+// lane 0 (Philox keyed by (seed, first + k)).
+__global__ void __launch_bounds__(256) placement_moves_kernel(const uint8_t* __restrict__ base, int64_t per_base,
+                                                              const uint8_t* __restrict__ allowed, int D, int T,
+                                                              uint64_t seed, int64_t first, int64_t n, int max_moves,
+                                                              uint8_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (T % 16) == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  for (int64_t k = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; k < n; k += nw) {
+    const uint8_t* src = base + (k / per_base) * T;
+    uint8_t* dst = out + k * T;
+    if (vec) {
+      for (int i = lane; i < T / 16; i += 32)
+        reinterpret_cast<uint4*>(dst)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    } else {
+      for (int i = lane; i < T; i += 32) dst[i] = src[i];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      Philox rng(seed, static_cast<uint64_t>(first + k), 0x4u);
+      const int nm = 1 + rng.below(max_moves);
+      for (int m = 0; m < nm; ++m) {
+        const int i = rng.below(T), d = rng.below(D);
+        if (allowed[i * D + d]) dst[i] = static_cast<uint8_t>(d);
+      }
+    }
+    __syncwarp();
+  }
+}
 }  // namespace
 
 void random_placements_device(const xe_problem* pr, uint64_t seed, int64_t first, int64_t n, uint8_t* out,
@@ -716,6 +751,27 @@ void move_cubes_device(const xe_problem* pr, const uint32_t* base, int64_t n_bas
     move_kernel<<<grid, kRoundWarps * 32, smem, s>>>(a);
     XE_CUDA(cudaGetLastError());
   }
+}
+
+void move_placements_device(const xe_problem* pr, const uint8_t* base, int64_t n_base, uint64_t seed, int64_t first,
+                            int64_t n, int max_moves, uint8_t* out, cudaStream_t s) {
+  const HostProblem& h = pr->h;
+  std::vector<uint8_t> allowed(static_cast<size_t>(h.T) * h.D, 0);
+  for (int i = 0; i < h.T; ++i)
+    for (int d = 0; d < h.D; ++d)
+      allowed[static_cast<size_t>(i) * h.D + d] = h.cost[static_cast<size_t>(d) * h.T + i] < 1.0e9 ? 1 : 0;
+  DevBuf<uint8_t> d_allowed;
+  d_allowed.upload(allowed, s);
+  int nsm = 0;
+  XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+  if (n > 0) {
+    const int64_t want = (n + 7) / 8;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(nsm) * 16)));
+    placement_moves_kernel<<<grid, 256, 0, s>>>(base, std::max<int64_t>(1, n / std::max<int64_t>(1, n_base)),
+                                                d_allowed.p, h.D, h.T, seed, first, n, max_moves, out);
+    XE_CUDA(cudaGetLastError());
+  }
+  XE_CUDA(cudaStreamSynchronize(s));  // the allowed table is call-local
 }
 
 }  // namespace xe

@@ -147,15 +147,13 @@ def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 2
     capped at 4e6 placements) cannot go — config 5 has 8^2000: K2b scores
     `n_random` uniform placements (xe_random_placements), the best distinct
     valid ones seed `chains` iterated local searches whose neighbours change
-    the device of 1..max_moves random ops (to a device that can run them);
+    the device of 1..max_moves random ops (to a device that can run them;
+    K4 xe_move_placements);
     each iteration scores chains x chain_n neighbours exactly (K2b) and a
     chain moves to its best valid neighbour when it improves, or after
     `stall` iterations without improvement."""
     import torch
-    from .api import evaluate_placements, random_placements
-    T, D = problem.T, problem.D
-    a = problem.arrays()
-    allowed = torch.from_numpy(np.asarray(a["cost_ms"]).reshape(D, T).T < 1e9).cuda()  # [T, D]
+    from .api import evaluate_placements, move_placements, random_placements
     dev = random_placements(problem, n_random, seed)
     r = evaluate_placements(problem, dev, policy=policy, valid_mask=valid_mask)
     score = torch.where((r.flags & valid_mask) == 0, r.obj, torch.full_like(r.obj, float("inf")))
@@ -176,22 +174,14 @@ def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 2
     bases, cur = dev[sel].clone(), score[sel].clone()
     del dev, r, score
     P, M = chains, chain_n
-    g = torch.Generator(device="cuda")
-    g.manual_seed(seed)
     stalled = torch.zeros(P, dtype=torch.int32, device="cuda")
     rows = torch.arange(P, device="cuda") * M
     best = float(cur.min().item())
     best_dev = bases[int(torch.argmin(cur))].clone()
     improvements, n_eval = 0, n_random
-    cols = torch.arange(max_moves, device="cuda")
-    for _ in range(iters):
-        nb = bases.repeat_interleave(M, dim=0)
-        nm = torch.randint(1, max_moves + 1, (P * M, 1), device="cuda", generator=g)
-        pos = torch.randint(0, T, (P * M, max_moves), device="cuda", generator=g)
-        new = torch.randint(0, D, (P * M, max_moves), device="cuda", generator=g, dtype=torch.int64)
-        ok = (cols[None, :] < nm) & allowed[pos, new]
-        cur_dev = torch.gather(nb, 1, pos).to(torch.int64)
-        nb.scatter_(1, pos, torch.where(ok, new, cur_dev).to(torch.uint8))
+    nb = torch.empty((P * M, problem.T), dtype=torch.uint8, device="cuda")
+    for it in range(iters):
+        move_placements(problem, bases, P * M, seed ^ 0x9E3779B9, first=it * P * M, max_moves=max_moves, out=nb)
         r = evaluate_placements(problem, nb, policy=policy, valid_mask=valid_mask, best=False)
         n_eval += P * M
         s = torch.where((r.flags & valid_mask) == 0, r.obj, torch.full_like(r.obj, float("inf"))).view(P, M)
@@ -205,7 +195,7 @@ def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 2
         if b < best:
             best, best_dev = b, bases[int(torch.argmin(cur))].clone()
             improvements += 1
-        del nb, r, s
+        del r, s
     r1 = evaluate_placements(problem, best_dev.unsqueeze(0).contiguous(), policy=policy, valid_mask=valid_mask)
     assert r1.best_obj == best, (r1.best_obj, best)
     return PlacementSearchResult(best, best_dev.cpu().numpy(), r1.peak.cpu().numpy()[0], rand_best, n_eval,
