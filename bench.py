@@ -318,10 +318,16 @@ def main():
     il = torch.empty(((n + 31) // 32) * 32 * il_words_per_cand, dtype=torch.int64, device="cuda")
     chunk = 1 << 20
     tmp = torch.empty((chunk, prob.cube_words), dtype=torch.int32, device="cuda")
+    gen_ms = 0.0  # K4 generation of the workload (not part of the timed steps)
     for lo in range(0, n, chunk):
         m = min(chunk, n - lo)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
         xe.round_cubes(prob, m, SEED, first=rank * n + lo, edits=3, perturb=0.1, out=tmp[:m])
+        g1.record()
         xe.cubes_to_il(prob, tmp[:m], out=il[lo * il_words_per_cand:])
+        torch.cuda.synchronize()
+        gen_ms += g0.elapsed_time(g1)
     del tmp
     obj = torch.empty(n, dtype=torch.float64, device="cuda")
     pk = torch.empty((n, D), dtype=torch.int64, device="cuda")
@@ -396,6 +402,8 @@ def main():
                      "bytes_per_candidate": bytes_per_cand},
         "clocks": clocks,
         "gpu_launches": 2 * args.steps,
+        "k4_generation": {"what": "K4 round_cubes of this workload (placement + minimal-save + 3 edits + 10 % flips)",
+                          "candidates_per_s": n / (gen_ms / 1e3) if gen_ms > 0 else None, "ms": gen_ms},
     }
 
     # ---- end-to-end: host (pinned) cubes through the C ABI, best read back ----
