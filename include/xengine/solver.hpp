@@ -57,7 +57,7 @@ struct SearchParams {
 // rounding with canonical saves -> K2 exact scoring (objective_value of the
 // completion, check_assignment, integer budgets, decode legality) -> R-space
 // local-search population.  backend "b200"; status Optimal when the
-// objective meets the LP lower bound (to 1e-9 relative), LimitReached
+// objective meets the LP lower bound (to the PDHG tolerance, 1e-6 relative), LimitReached
 // otherwise (objective NaN and an empty assignment when no valid schedule
 // was found: infeasibility is not proven); nodes_explored = candidates
 // scored.  The assignment is complete_assignment of the best (R, S).

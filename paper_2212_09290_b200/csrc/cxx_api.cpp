@@ -937,7 +937,9 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
     s.objective_ms = std::numeric_limits<double>::quiet_NaN();
     return s;
   }
-  const bool proven = r.has_lp && r.objective <= r.lp_bound + 1e-9 * std::max(1.0, std::fabs(r.objective));
+  // the LP value carries the PDHG tolerance (xe_search_opts.lp_tol, 1e-6
+  // relative): the schedule is optimal to that tolerance when it meets it
+  const bool proven = r.has_lp && r.objective <= r.lp_bound + so.lp_tol * std::max(1.0, std::fabs(r.objective));
   s.status = proven ? SolveStatus::Optimal : SolveStatus::LimitReached;
   s.objective_ms = r.objective;
   BitCube R(D, T), S(D, T);
