@@ -52,6 +52,22 @@ def traffic_from_profiles(config, n):
     return None
 
 
+def issue_roofline(config, cand_per_s, clocks):
+    """What bounds K2a: warp-instructions issued per candidate (committed ncu
+    capture) x candidates/s against the SM issue peak (148 SMs x 4 schedulers
+    x 1 warp-instruction per clock at the sampled SM clock)."""
+    p = os.path.join(ROOT, "profiles", "k2a_traffic.json")
+    d = json.load(open(p)).get(config) if os.path.exists(p) else None
+    if not d or "warp_instructions_per_candidate" not in d:
+        return None
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    achieved = d["warp_instructions_per_candidate"] * cand_per_s
+    return {"bound": "issue", "unit": "warp-instructions/s", "achieved": achieved, "peak": peak,
+            "frac": achieved / peak, "warp_instructions_per_candidate": d["warp_instructions_per_candidate"],
+            "ncu_issue_active_pct": d.get("issue_active_pct")}
+
+
 def cpu_reference_rate(doc, a, seconds=12.0, nthreads=None, cubes=None):
     """Reference library (oracle/_ref) on the host cores: per candidate
     complete_assignment + objective_value + check_assignment + peaks."""
@@ -399,7 +415,8 @@ def main():
                      "frac": achieved / hbm, "traffic": traffic_from_profiles("vgg16", n), "traffic_unit": "GB per launch",
                      "algorithmic_gb_per_launch": n * bytes_per_cand / 1e9,
                      "peak_kind": peak_kind, "kernel_ms": kern_ms,
-                     "bytes_per_candidate": bytes_per_cand},
+                     "bytes_per_candidate": bytes_per_cand,
+                     "issue": issue_roofline("vgg16", n / (kern_ms / 1e3), clocks)},
         "clocks": clocks,
         "gpu_launches": 2 * args.steps,
         "k4_generation": {"what": "K4 round_cubes of this workload (placement + minimal-save + 3 edits + 10 % flips)",
