@@ -153,3 +153,20 @@ def test_move_cubes_neighbours(oracle):
     r = xe.evaluate_cubes(prob, nb, xe.ModelOptions(strict_free=True), valid_mask=0)
     assert np.array_equal(r.obj.cpu().numpy().view(np.int64), o.view(np.int64))
     assert np.array_equal(r.flags.cpu().numpy().astype(np.uint32), f)
+
+
+def test_move_placements_neighbours():
+    # K4 placement moves: copies of the base with <= max_moves ops moved, only
+    # to devices that can run them (fig2: op 0 never on the gpu), deterministic
+    prob = xe.Problem.from_json(golden_problem_text("fig2"))
+    cost = prob.arrays()["cost_ms"]
+    base = torch.tensor([[0, 1, 1, 1, 1, 1, 0], [0, 0, 0, 0, 0, 0, 0]], dtype=torch.uint8, device="cuda")
+    nb = xe.move_placements(prob, base, 2 * 4096, seed=5, max_moves=3)
+    assert torch.equal(nb, xe.move_placements(prob, base, 2 * 4096, seed=5, max_moves=3))
+    h = nb.cpu().numpy()
+    b = base.cpu().numpy()
+    diff = (h != np.repeat(b, 4096, axis=0)).sum(1)
+    assert diff.max() <= 3 and (diff > 0).mean() > 0.5
+    allowed = cost.T < 1e9  # [T, D]
+    assert allowed[np.arange(prob.T)[None, :], h].all()
+    assert (h[:, 0] == 0).all()
