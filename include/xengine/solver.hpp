@@ -47,7 +47,7 @@ struct SearchParams {
   bool use_lp = true;       // LP-guided rounding and the LP lower bound
   int chains = 256;         // local-search population (0: rounding only)
   int chain_neighbours = 1024;
-  int chain_iters = 100;
+  int chain_iters = 200;
   int max_moves = 4;
   int stall = 15;
   SearchLimits limits;      // time_limit_ms honoured (node_limit: candidates are not nodes)

@@ -357,7 +357,7 @@ typedef struct xe_search_opts {
                             local search are skipped when a cube does not fit the move kernel) */
   int32_t chains;        /* local-search population (256; 0 = rounding only) */
   int32_t chain_n;       /* neighbours per chain per iteration (1024) */
-  int32_t chain_iters;   /* iterations (100) */
+  int32_t chain_iters;   /* iterations (200) */
   int32_t max_moves;     /* moves per neighbour, 1..max_moves (4) */
   int32_t stall;         /* iterations without improvement before a kick (15) */
   int64_t first;         /* global index of the first rounded candidate (0) */

@@ -32,6 +32,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "csr.hpp"
 
 namespace xe {
@@ -49,6 +51,18 @@ __host__ __device__ inline double score(double obj, uint32_t flags, uint32_t mas
   for (int d = 0; d < D; ++d)
     if (peak[d] > budget[d]) ex += static_cast<double>(peak[d] - budget[d]) / static_cast<double>(budget[d] > 0 ? budget[d] : 1);
   return kOverBudget + ex;
+}
+
+// scores of a rounding batch as sortable keys (non-negative doubles order as
+// their bit patterns), with their indices
+__global__ void score_keys_kernel(const double* __restrict__ obj, const uint32_t* __restrict__ flags,
+                                  const int64_t* __restrict__ peak, const int64_t* __restrict__ budget, int D,
+                                  uint32_t mask, int64_t n, uint64_t* __restrict__ key, int32_t* __restrict__ idx) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    key[i] = static_cast<uint64_t>(__double_as_longlong(score(obj[i], flags[i], mask, peak + i * D, budget, D)));
+    idx[i] = static_cast<int32_t>(i);
+  }
 }
 
 // best-scoring neighbour of every chain: one warp per chain, lowest index on ties
@@ -171,9 +185,9 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
   std::vector<double> pool_obj;  // the population: best distinct objectives
   DevBuf<uint32_t> pool;
   pool.alloc(static_cast<size_t>(std::max(1, chains)) * words);
-  std::vector<double> ho;
-  std::vector<uint32_t> hf;
-  std::vector<int64_t> hp;
+  DevBuf<uint64_t> keys, keys_out;
+  DevBuf<int32_t> kidx, kidx_out;
+  DevBuf<unsigned char> sort_tmp;
   auto candidates = [&](int64_t lo, int64_t cnt, uint32_t* out) {
     check_rc(xe_round_cubes(pr, so.use_lp ? x.p : nullptr, so.seed, lo, cnt, so.edits, 0.0, out, s));
     if (canonical) check_rc(xe_move_cubes(pr, out, cnt, 0, 0, cnt, 0, out, s));
@@ -195,20 +209,38 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
       res->index = lo + b.index;
     }
     if (chains <= 0) continue;
-    // merge the batch's best distinct scores into the population
-    ho.resize(static_cast<size_t>(n));
-    hf.resize(static_cast<size_t>(n));
-    hp.resize(static_cast<size_t>(n) * h.D);
-    XE_CUDA(cudaMemcpyAsync(ho.data(), obj.p, n * 8, cudaMemcpyDeviceToHost, s));
-    XE_CUDA(cudaMemcpyAsync(hf.data(), flags.p, n * 4, cudaMemcpyDeviceToHost, s));
-    XE_CUDA(cudaMemcpyAsync(hp.data(), peak.p, n * h.D * 8, cudaMemcpyDeviceToHost, s));
+    // merge the batch's best distinct scores into the population: scores
+    // sorted on the device (stable radix sort: ties keep index order), only
+    // the head comes back
+    {
+      keys.reserve(static_cast<size_t>(n));
+      keys_out.reserve(static_cast<size_t>(n));
+      kidx.reserve(static_cast<size_t>(n));
+      kidx_out.reserve(static_cast<size_t>(n));
+      const int g = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+      score_keys_kernel<<<g, 256, 0, s>>>(obj.p, flags.p, peak.p, pr->d_budget.p, h.D, mask, n, keys.p, kidx.p);
+      XE_CUDA(cudaGetLastError());
+      size_t tb = 0;
+      XE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_out.p, kidx.p, kidx_out.p,
+                                              static_cast<int>(n), 0, 64, s));
+      sort_tmp.reserve(std::max<size_t>(1, tb));
+      XE_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tb, keys.p, keys_out.p, kidx.p, kidx_out.p,
+                                              static_cast<int>(n), 0, 64, s));
+    }
+    // enough of the head for `chains` distinct scores (rounding repeats schedules)
+    const int64_t head = std::min<int64_t>(n, 256 * static_cast<int64_t>(chains));
+    std::vector<uint64_t> hk(static_cast<size_t>(head));
+    std::vector<int32_t> hi(static_cast<size_t>(head));
+    XE_CUDA(cudaMemcpyAsync(hk.data(), keys_out.p, head * 8, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaMemcpyAsync(hi.data(), kidx_out.p, head * 4, cudaMemcpyDeviceToHost, s));
     XE_CUDA(cudaStreamSynchronize(s));
     std::vector<Cand> c;
     for (int i = 0; i < static_cast<int>(pool_obj.size()); ++i) c.push_back({pool_obj[static_cast<size_t>(i)], -1 - i});
-    for (int64_t i = 0; i < n; ++i) {
-      const size_t q = static_cast<size_t>(i);
-      const double v = score(ho[q], hf[q], mask, hp.data() + q * h.D, h.budget.data(), h.D);
-      if (v < INFINITY) c.push_back({v, i});
+    for (int64_t q = 0; q < head; ++q) {
+      double v;
+      std::memcpy(&v, &hk[static_cast<size_t>(q)], 8);
+      if (!(v < INFINITY)) break;
+      c.push_back({v, hi[static_cast<size_t>(q)]});
     }
     // pool entries first among equal objectives (they are older, lower index)
     std::stable_sort(c.begin(), c.end(), [](const Cand& a, const Cand& b) { return a.obj < b.obj; });
@@ -325,7 +357,7 @@ extern "C" void xe_search_opts_default(xe_search_opts* o) {
   o->canonical = 1;
   o->chains = 256;
   o->chain_n = 1024;
-  o->chain_iters = 100;
+  o->chain_iters = 200;
   o->max_moves = 4;
   o->stall = 15;
   o->first = 0;

@@ -64,7 +64,7 @@ class SearchResult:
 def search(problem: Problem, opts: Optional[ModelOptions] = None, n_per_round: int = 1 << 18,
            rounds: int = 4, seed: int = 1, edits: int = 3, use_lp: bool = True,
            valid_mask: int = DEFAULT_MASK, first: int = 0, lp_tol: float = 1e-6,
-           distributed: bool = False, chains: int = 256, chain_n: int = 1024, chain_iters: int = 100,
+           distributed: bool = False, chains: int = 256, chain_n: int = 1024, chain_iters: int = 200,
            max_moves: int = 4, stall: int = 15, canonical: bool = True,
            time_limit_ms: int = 0) -> SearchResult:
     """One native call (xe_search, csrc/search.cu) per GPU.

@@ -140,7 +140,7 @@ def test_search_abi_defaults_and_argument_checks():
     _lib.LIB.xe_search_opts_default(C.byref(o))
     assert (o.n_per_round, o.rounds, o.edits, o.seed, o.use_lp) == (1 << 18, 4, 3, 1, 1)
     assert o.valid_mask == (_lib.F_CHECK_MASK | _lib.F_BUDGET | _lib.F_DECODE)
-    assert (o.canonical, o.chains, o.chain_n, o.chain_iters, o.max_moves, o.stall) == (1, 256, 1024, 100, 4, 15)
+    assert (o.canonical, o.chains, o.chain_n, o.chain_iters, o.max_moves, o.stall) == (1, 256, 1024, 200, 4, 15)
     assert (o.first, o.rank, o.world, o.time_limit_ms) == (0, 0, 1, 0)
     r = _lib.SearchResult()
     rc = _lib.LIB.xe_search(None, None, C.byref(o), C.byref(r), None, None, None)
