@@ -215,8 +215,18 @@ int xe_csr_last_build_ms(const xe_csr* m, float* ms);
  * (model.hpp:127-139).  Bytes per candidate: 8*D*T*W. */
 size_t xe_cube_bytes(int32_t D, int32_t T);
 
+/* Objective order.  objective_value (model.cpp:369-428) sums its terms
+ * sequentially in (d,t,i) then (t,e,dc,ds) order.  The streaming evaluator
+ * sums them per timestep: xe_eval_out.obj is that reassociation, within
+ * (#terms * 2^-53) relative of the reference (north_star tolerance 1e-6),
+ * and bit-identical to it when xe_objective_order_exact() reports 1 (every
+ * term dyadic: every partial sum exact in any order).  xe_best.obj/index
+ * are always exact: the near-best candidates are re-scored in the
+ * reference's order and the first minimum of those bits wins. */
+int xe_objective_order_exact(const struct xe_problem* p, int32_t* exact);
+
 typedef struct xe_eval_out {
-  double* obj;      /* [n] objective_value of the completion (model.cpp:369-428) */
+  double* obj;      /* [n] objective_value of the completion (model.cpp:369-428), see above */
   int64_t* peak;    /* [n][D] max_t,v U(d,t,v) = replay peaks (schedule.cpp:326-367) */
   uint32_t* flags;  /* [n] XE_F_* bits */
 } xe_eval_out;
@@ -240,14 +250,15 @@ int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t
 int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                        int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best);
 
-/* Candidate-interleaved layout ("xe_cube_il", T <= 64, D <= 8): the native
- * layout of the lane-per-candidate evaluator.  u64 bit row (which, d, t) of
- * candidate c (which 0 = R, 1 = S) is at
- *     il[((c / 32) * K + (which * D + d) * T + t) * 32 + c % 32],  K = 2*D*T,
- * so a warp reading one row of 32 candidates touches one 256-byte line.
- * Buffers hold ceil(n/32)*32 candidates (padding lanes are ignored).
- * xe_eval_cubes / xe_eval_cubes_host transpose canonical cubes into this
- * layout internally when T <= 64. */
+/* Candidate-interleaved layout ("xe_cube_il", T <= 256, D <= 8): the native
+ * layout of the lane-per-candidate evaluators.  With NW = ceil(T/64) u64
+ * words per bit row, word j of row (which, d, t) of candidate c (which 0 =
+ * R, 1 = S; bit i of word j = operator 64j+i) is at
+ *     il[((c / 32) * K + ((which * D + d) * T + t) * NW + j) * 32 + c % 32],
+ * K = 2*D*T*NW, so a warp reading one word of 32 candidates touches one
+ * 256-byte line.  Buffers hold ceil(n/32)*32 candidates (padding lanes are
+ * ignored).  xe_eval_cubes / xe_eval_cubes_host transpose canonical cubes
+ * into this layout internally. */
 size_t xe_cube_il_bytes(int32_t D, int32_t T, int64_t n);
 /* canonical device cubes [n] -> interleaved device buffer (xe_cube_il_bytes) */
 int xe_cubes_to_il(const xe_problem* p, const uint32_t* cubes, int64_t n, uint64_t* il, void* stream);

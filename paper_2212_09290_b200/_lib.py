@@ -153,6 +153,7 @@ SIGNATURES = {
     "xe_eval_cubes_host": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, C.POINTER(EvalOut),
                                      C.c_uint32, C.POINTER(Best)]),
     "xe_cube_il_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int64]),
+    "xe_objective_order_exact": (C.c_int, [P, C.POINTER(C.c_int32)]),
     "xe_cubes_to_il": (C.c_int, [P, P, C.c_int64, P, P]),
     "xe_eval_cubes_il": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, C.POINTER(EvalOut),
                                    C.c_uint32, C.POINTER(Best), P]),

@@ -138,6 +138,16 @@ class Problem:
     def cube_words(self) -> int:
         return 2 * self.D * self.T * ((self.T + 31) // 32)
 
+    @property
+    def objective_order_exact(self) -> bool:
+        """True when per-candidate objectives are bit-identical to the
+        reference's sequential sum (every term dyadic); otherwise they are a
+        per-timestep reassociation within ~#terms * 2^-53 relative.  The
+        best-of-batch objective is exact either way."""
+        x = C.c_int32()
+        check(LIB.xe_objective_order_exact(self._h, C.byref(x)))
+        return bool(x.value)
+
 
 @dataclass
 class EvalResult:

@@ -130,7 +130,9 @@ int64_t stage_chunk(const HostProblem& h) {
 
 // Best over per-chunk (objective bits, chunk-local index, valid count)
 // triples; chunks ascend in candidate index, so a strict < keeps the first.
-void combine_chunks(const uint64_t* dev, int64_t nchunks, int64_t chunk, cudaStream_t s, xe_best* best) {
+// Returns false when a chunk reports more near-ties than the exact re-score
+// holds (index -2): the caller re-runs the batch with the exact kernels.
+bool combine_chunks(const uint64_t* dev, int64_t nchunks, int64_t chunk, cudaStream_t s, xe_best* best) {
   std::vector<uint64_t> hb(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
   if (nchunks) {
     XE_CUDA(cudaMemcpyAsync(hb.data(), dev, static_cast<size_t>(nchunks) * 24, cudaMemcpyDeviceToHost, s));
@@ -142,6 +144,7 @@ void combine_chunks(const uint64_t* dev, int64_t nchunks, int64_t chunk, cudaStr
   uint64_t bk = ~0ull;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t idx = static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 1)]);
+    if (idx == -2) return false;
     best->n_valid += static_cast<int64_t>(hb[static_cast<size_t>(3 * c + 2)]);
     if (idx >= 0 && hb[static_cast<size_t>(3 * c)] < bk) {
       bk = hb[static_cast<size_t>(3 * c)];
@@ -149,6 +152,7 @@ void combine_chunks(const uint64_t* dev, int64_t nchunks, int64_t chunk, cudaStr
       std::memcpy(&best->obj, &bk, 8);
     }
   }
+  return true;
 }
 
 }  // namespace
@@ -276,40 +280,60 @@ int xe_problem_with_budgets(const xe_problem* p, const int64_t* budgets, xe_prob
   });
 }
 
+// Canonical device cubes, chunk by chunk through the interleaved staging
+// buffer.  exact = the reference-order kernels (energy model; fallback).
+static void eval_canon_chunks(const xe_problem* p, const xe_model_opts& o, const uint32_t* cubes, int64_t n,
+                              xe_eval_out* out, uint32_t valid_mask, xe_best* best, cudaStream_t s, bool exact) {
+  auto* mp = const_cast<xe_problem*>(p);
+  const HostProblem& h = p->h;
+  double* obj = out ? out->obj : nullptr;
+  int64_t* peak = out ? out->peak : nullptr;
+  uint32_t* flags = out ? out->flags : nullptr;
+  const bool fast = !exact && stream_supported(p, o);
+  if (!fast && !il_supported(p)) {  // T > 64, exact: the warp-per-candidate kernel on the canonical layout
+    uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
+    eval_cubes_device(p, o, cubes, n, obj, peak, flags, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+    if (best) read_best(best3, s, best);
+    return;
+  }
+  const size_t cw = xe_cube_bytes(h.D, h.T) / 4;
+  const int64_t chunk = stage_chunk(h);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  auto& st = mp->stage[0];
+  const int64_t cap = std::min(chunk, std::max<int64_t>(n, 1));
+  st.il.reserve(il_bytes(h.D, h.T, cap) / 8);
+  if (best) mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+  const bool refine = fast && best && !stream_objective_exact(p);
+  if (refine && !obj) st.obj.reserve(static_cast<size_t>(cap));
+  if (refine && !flags) st.flags.reserve(static_cast<size_t>(cap));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+    uint64_t* b3 = best ? mp->chunk_best.p + 3 * c : nullptr;
+    cubes_to_il_device(p, cubes + lo * cw, m, st.il.p, s);
+    if (fast) {
+      double* o_obj = obj ? obj + lo : (refine ? st.obj.p : nullptr);
+      uint32_t* o_fl = flags ? flags + lo : (refine ? st.flags.p : nullptr);
+      eval_stream_device(p, o, st.il.p, m, o_obj, peak ? peak + lo * h.D : nullptr, o_fl, valid_mask, b3,
+                         mp->scratch.p, s);
+      if (refine)
+        refine_best_device(p, o, nullptr, cubes + lo * cw, m, o_obj, o_fl, valid_mask, b3, st.refine, mp->scratch.p,
+                           s);
+    } else {
+      eval_il_device(p, o, st.il.p, m, obj ? obj + lo : nullptr, peak ? peak + lo * h.D : nullptr,
+                     flags ? flags + lo : nullptr, valid_mask, b3, mp->scratch.p, s);
+    }
+  }
+  if (best && !combine_chunks(mp->chunk_best.p, nchunks, chunk, s, best))
+    eval_canon_chunks(p, o, cubes, n, out, valid_mask, best, s, true);  // > kRefineCap near-ties
+}
+
 int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes, int64_t n,
                   xe_eval_out* out, uint32_t valid_mask, xe_best* best, void* stream) {
   return guard([&] {
     if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
     require_uploaded(p);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
-    xe_model_opts o = opts_or_default(opts);
-    auto* mp = const_cast<xe_problem*>(p);
-    uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
-    double* obj = out ? out->obj : nullptr;
-    int64_t* peak = out ? out->peak : nullptr;
-    uint32_t* flags = out ? out->flags : nullptr;
-    if (!il_supported(p)) {  // T > 64: the warp-per-candidate kernel on the canonical layout
-      eval_cubes_device(p, o, cubes, n, obj, peak, flags, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
-      if (best) read_best(best3, s, best);
-      return;
-    }
-    // canonical -> interleaved in chunks of a stream-ordered staging buffer,
-    // then the lane-per-candidate evaluator
-    const HostProblem& h = p->h;
-    const size_t cw = xe_cube_bytes(h.D, h.T) / 4;
-    const int64_t chunk = stage_chunk(h);
-    const int64_t nchunks = (n + chunk - 1) / chunk;
-    auto& st = mp->stage[0];
-    st.il.reserve(il_bytes(h.D, h.T, std::min(chunk, std::max<int64_t>(n, 1))) / 8);
-    if (best) mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
-      cubes_to_il_device(p, cubes + lo * cw, m, st.il.p, s);
-      eval_il_device(p, o, st.il.p, m, obj ? obj + lo : nullptr, peak ? peak + lo * h.D : nullptr,
-                     flags ? flags + lo : nullptr, valid_mask, best ? mp->chunk_best.p + 3 * c : nullptr,
-                     mp->scratch.p, s);
-    }
-    if (best) combine_chunks(mp->chunk_best.p, nchunks, chunk, s, best);
+    eval_canon_chunks(p, opts_or_default(opts), cubes, n, out, valid_mask, best, static_cast<cudaStream_t>(stream),
+                      false);
   });
 }
 
@@ -321,14 +345,61 @@ int xe_eval_cubes_il(const xe_problem* p, const xe_model_opts* opts, const uint6
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     xe_model_opts o = opts_or_default(opts);
     auto* mp = const_cast<xe_problem*>(p);
+    const HostProblem& h = p->h;
     uint64_t* best3 = reinterpret_cast<uint64_t*>(mp->scratch.p + mp->scratch.n - 64);
-    eval_il_device(p, o, il, n, out ? out->obj : nullptr, out ? out->peak : nullptr, out ? out->flags : nullptr,
-                   valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
-    if (best) read_best(best3, s, best);
+    double* obj = out ? out->obj : nullptr;
+    int64_t* peak = out ? out->peak : nullptr;
+    uint32_t* flags = out ? out->flags : nullptr;
+    auto exact = [&] {  // reference-order kernels over the whole batch
+      if (il_supported(p)) {
+        eval_il_device(p, o, il, n, obj, peak, flags, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+        if (best) read_best(best3, s, best);
+        return;
+      }
+      // T > 64: convert to canonical chunk by chunk and use the v3 kernel
+      const size_t cw = xe_cube_bytes(h.D, h.T) / 4;
+      const int64_t chunk = stage_chunk(h), nchunks = (n + chunk - 1) / chunk;
+      auto& st = mp->stage[0];
+      st.canon.reserve(static_cast<size_t>(std::min(chunk, std::max<int64_t>(n, 1))) * cw);
+      if (best) mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+        il_to_canon_device(p, il, lo, m, st.canon.p, s);
+        eval_cubes_device(p, o, st.canon.p, m, obj ? obj + lo : nullptr, peak ? peak + lo * h.D : nullptr,
+                          flags ? flags + lo : nullptr, valid_mask, best ? mp->chunk_best.p + 3 * c : nullptr,
+                          mp->scratch.p, s);
+      }
+      if (best) combine_chunks(mp->chunk_best.p, nchunks, chunk, s, best);
+    };
+    if (!stream_supported(p, o)) {
+      if (!il_supported(p) && o.use_energy && h.has_energy)
+        fail(XE_ERR_TOO_LARGE, "interleaved cubes with the energy model need T <= 64");
+      exact();
+      return;
+    }
+    const bool refine = best && !stream_objective_exact(p);
+    auto& st = mp->stage[0];
+    if (refine && !obj) st.obj.reserve(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    if (refine && !flags) st.flags.reserve(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    double* o_obj = obj ? obj : (refine ? st.obj.p : nullptr);
+    uint32_t* o_fl = flags ? flags : (refine ? st.flags.p : nullptr);
+    eval_stream_device(p, o, il, n, o_obj, peak, o_fl, valid_mask, best ? best3 : nullptr, mp->scratch.p, s);
+    if (refine) refine_best_device(p, o, il, nullptr, n, o_obj, o_fl, valid_mask, best3, st.refine, mp->scratch.p, s);
+    if (best) {
+      read_best(best3, s, best);
+      if (best->index == -2) exact();  // more than kRefineCap near-ties
+    }
   });
 }
 
 size_t xe_cube_il_bytes(int32_t D, int32_t T, int64_t n) { return il_bytes(D, T, n); }
+
+int xe_objective_order_exact(const xe_problem* p, int32_t* exact) {
+  return guard([&] {
+    if (!p || !exact) fail(XE_ERR_ARG, "null argument");
+    *exact = p->device >= 0 && stream_objective_exact(p) ? 1 : 0;
+  });
+}
 
 int xe_cubes_to_il(const xe_problem* p, const uint32_t* cubes, int64_t n, uint64_t* il, void* stream) {
   return guard([&] {
@@ -341,64 +412,80 @@ int xe_cubes_to_il(const xe_problem* p, const uint32_t* cubes, int64_t n, uint64
 // End-to-end path: host candidates in, host results out.  Chunks alternate
 // between two streams with their own staging buffers, so the host->device
 // copy of chunk k+1 overlaps the transpose + evaluation of chunk k.
+static void eval_host_chunks(const xe_problem* p, const xe_model_opts& o, const uint32_t* cubes, int64_t n,
+                             xe_eval_out* out, uint32_t valid_mask, xe_best* best, bool exact) {
+  auto* mp = const_cast<xe_problem*>(p);
+  const HostProblem& h = p->h;
+  const bool fast = !exact && stream_supported(p, o);
+  const bool il = fast || il_supported(p);
+  const bool refine = fast && !stream_objective_exact(p);
+  const size_t cb = xe_cube_bytes(h.D, h.T);
+  const int64_t chunk = il ? stage_chunk(h) : std::max<int64_t>(1024, static_cast<int64_t>((256ull << 20) / cb));
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const int64_t cap = std::min(chunk, std::max<int64_t>(n, 1));
+  const size_t sb = eval_scratch_bytes(p->device);
+  for (auto& st : mp->stage) {
+    if (!st.stream) XE_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
+    st.canon.reserve(static_cast<size_t>(cap) * cb / 4);
+    if (il) st.il.reserve(il_bytes(h.D, h.T, cap) / 8);
+    if ((out && out->obj) || refine) st.obj.reserve(static_cast<size_t>(cap));
+    if (out && out->peak) st.peak.reserve(static_cast<size_t>(cap) * h.D);
+    if ((out && out->flags) || refine) st.flags.reserve(static_cast<size_t>(cap));
+    st.scratch.reserve(sb);
+  }
+  mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
+  // the two stages' streams must not start before work already queued on
+  // the handle's stream (previous calls) has finished with the buffers
+  XE_CUDA(cudaStreamSynchronize(p->stream));
+  try {
+    for (int64_t c = 0; c < nchunks; ++c) {
+      auto& st = mp->stage[c & 1];
+      const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+      uint64_t* b3 = mp->chunk_best.p + 3 * c;
+      h2d(st.canon.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
+          st.stream);
+      double* o_obj = (out && out->obj) || refine ? st.obj.p : nullptr;
+      uint32_t* o_fl = (out && out->flags) || refine ? st.flags.p : nullptr;
+      if (fast) {
+        cubes_to_il_device(p, st.canon.p, m, st.il.p, st.stream);
+        eval_stream_device(p, o, st.il.p, m, o_obj, st.peak.p, o_fl, valid_mask, b3, st.scratch.p, st.stream);
+        if (refine)
+          refine_best_device(p, o, nullptr, st.canon.p, m, o_obj, o_fl, valid_mask, b3, st.refine, st.scratch.p,
+                             st.stream);
+      } else if (il) {
+        cubes_to_il_device(p, st.canon.p, m, st.il.p, st.stream);
+        eval_il_device(p, o, st.il.p, m, o_obj, st.peak.p, o_fl, valid_mask, b3, st.scratch.p, st.stream);
+      } else {
+        eval_cubes_device(p, o, st.canon.p, m, o_obj, st.peak.p, o_fl, valid_mask, b3, st.scratch.p, st.stream);
+      }
+      if (out && out->obj)
+        XE_CUDA(cudaMemcpyAsync(out->obj + lo, st.obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st.stream));
+      if (out && out->peak)
+        XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, st.peak.p, m * h.D * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                st.stream));
+      if (out && out->flags)
+        XE_CUDA(cudaMemcpyAsync(out->flags + lo, st.flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                st.stream));
+    }
+    XE_CUDA(cudaStreamSynchronize(mp->stage[0].stream));
+    XE_CUDA(cudaStreamSynchronize(mp->stage[1].stream));
+  } catch (...) {
+    cudaStreamSynchronize(mp->stage[0].stream);
+    cudaStreamSynchronize(mp->stage[1].stream);
+    throw;
+  }
+  if (best && !combine_chunks(mp->chunk_best.p, nchunks, chunk, p->stream, best))
+    eval_host_chunks(p, o, cubes, n, out, valid_mask, best, true);  // > kRefineCap near-ties
+}
+
 int xe_eval_cubes_host(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                        int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best) {
   return guard([&] {
     if (!p || (!cubes && n > 0) || n < 0) fail(XE_ERR_ARG, "null argument");
     require_uploaded(p);
     xe_model_opts o = opts_or_default(opts);
-    auto* mp = const_cast<xe_problem*>(p);
-    const HostProblem& h = p->h;
-    const bool il = il_supported(p);
-    const size_t cb = xe_cube_bytes(h.D, h.T);
-    const int64_t chunk = il ? stage_chunk(h) : std::max<int64_t>(1024, static_cast<int64_t>((256ull << 20) / cb));
-    const int64_t nchunks = (n + chunk - 1) / chunk;
-    const int64_t cap = std::min(chunk, std::max<int64_t>(n, 1));
-    const size_t sb = eval_scratch_bytes(p->device);
-    for (auto& st : mp->stage) {
-      if (!st.stream) XE_CUDA(cudaStreamCreateWithFlags(&st.stream, cudaStreamNonBlocking));
-      st.canon.reserve(static_cast<size_t>(cap) * cb / 4);
-      if (il) st.il.reserve(il_bytes(h.D, h.T, cap) / 8);
-      if (out && out->obj) st.obj.reserve(static_cast<size_t>(cap));
-      if (out && out->peak) st.peak.reserve(static_cast<size_t>(cap) * h.D);
-      if (out && out->flags) st.flags.reserve(static_cast<size_t>(cap));
-      st.scratch.reserve(sb);
-    }
-    mp->chunk_best.reserve(static_cast<size_t>(std::max<int64_t>(1, nchunks)) * 3);
-    // the two stages' streams must not start before work already queued on
-    // the handle's stream (previous calls) has finished with the buffers
-    XE_CUDA(cudaStreamSynchronize(p->stream));
-    try {
-      for (int64_t c = 0; c < nchunks; ++c) {
-        auto& st = mp->stage[c & 1];
-        const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
-        h2d(st.canon.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
-            st.stream);
-        if (il) {
-          cubes_to_il_device(p, st.canon.p, m, st.il.p, st.stream);
-          eval_il_device(p, o, st.il.p, m, st.obj.p, st.peak.p, st.flags.p, valid_mask, mp->chunk_best.p + 3 * c,
-                         st.scratch.p, st.stream);
-        } else {
-          eval_cubes_device(p, o, st.canon.p, m, st.obj.p, st.peak.p, st.flags.p, valid_mask,
-                            mp->chunk_best.p + 3 * c, st.scratch.p, st.stream);
-        }
-        if (out && out->obj)
-          XE_CUDA(cudaMemcpyAsync(out->obj + lo, st.obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st.stream));
-        if (out && out->peak)
-          XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, st.peak.p, m * h.D * sizeof(int64_t),
-                                  cudaMemcpyDeviceToHost, st.stream));
-        if (out && out->flags)
-          XE_CUDA(cudaMemcpyAsync(out->flags + lo, st.flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                  st.stream));
-      }
-      XE_CUDA(cudaStreamSynchronize(mp->stage[0].stream));
-      XE_CUDA(cudaStreamSynchronize(mp->stage[1].stream));
-    } catch (...) {
-      cudaStreamSynchronize(mp->stage[0].stream);
-      cudaStreamSynchronize(mp->stage[1].stream);
-      throw;
-    }
-    if (best) combine_chunks(mp->chunk_best.p, nchunks, chunk, p->stream, best);
+    xe_best tmp;
+    eval_host_chunks(p, o, cubes, n, out, valid_mask, best ? best : &tmp, false);
   });
 }
 

@@ -29,8 +29,9 @@
 // Pass A re-reads the R rows pass B just streamed; they come from L2, so
 // HBM sees each candidate once.  Built with -fmad=false.
 //
-// Also here: the canonical -> interleaved transpose used by the canonical
-// and host entry points (xe_eval_cubes, xe_eval_cubes_host).
+// This kernel keeps the reference's summation order term by term; it serves
+// the energy model and the exact re-score of the streaming evaluator's
+// best-of-batch (eval_stream.cu).
 
 #include "eval_cube_kernel.cuh"
 
@@ -534,35 +535,6 @@ __global__ void __launch_bounds__(kWarps * 32, MAXD <= 2 ? 3 : (MAXD <= 4 ? 2 : 
   }
 }
 
-// canonical [n][2*D*T*W32] u32 -> interleaved [ceil(n/32)][2*D*T][32] u64
-// (W32 <= 2).  One CTA per 32-candidate group, a 32x32 tile of u64 rows in
-// shared memory: coalesced reads along each cube, coalesced writes along
-// the candidates.
-__global__ void __launch_bounds__(256) to_il_kernel(const uint32_t* __restrict__ in, int64_t n, int K,
-                                                    int W32, uint64_t* __restrict__ out) {
-  __shared__ uint64_t tile[32][33];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t g = blockIdx.x;
-  for (int k0 = 0; k0 < K; k0 += 32) {
-    for (int j = wid; j < 32; j += 8) {
-      const int64_t c = g * 32 + j;
-      const int k = k0 + lane;
-      uint64_t v = 0;
-      if (c < n && k < K) {
-        const uint32_t* p = in + static_cast<size_t>(c) * K * W32 + static_cast<size_t>(k) * W32;
-        v = W32 == 2 ? *reinterpret_cast<const uint64_t*>(p) : static_cast<uint64_t>(*p);
-      }
-      tile[j][lane] = v;
-    }
-    __syncthreads();
-    for (int r = wid; r < 32; r += 8) {
-      const int k = k0 + r;
-      if (k < K) out[(static_cast<size_t>(g) * K + k) * 32 + lane] = tile[lane][r];
-    }
-    __syncthreads();
-  }
-}
-
 int align16(int x) { return (x + 15) & ~15; }
 
 template <int MAXD, class M>
@@ -591,20 +563,6 @@ void reduce_best_launch(const uint64_t* key, const int64_t* idx, const int64_t* 
                         cudaStream_t s);
 
 bool il_supported(const xe_problem* pr) { return pr->h.T <= 64 && pr->h.D <= 8; }
-
-size_t il_bytes(int D, int T, int64_t n) {
-  return static_cast<size_t>((n + 31) / 32) * 32 * 2 * D * T * 8;
-}
-
-void cubes_to_il_device(const xe_problem* pr, const uint32_t* cubes, int64_t n, uint64_t* il, cudaStream_t s) {
-  const HostProblem& h = pr->h;
-  if (!il_supported(pr)) fail(XE_ERR_TOO_LARGE, "interleaved cubes need T <= 64 and D <= 8");
-  const int64_t ngroups = (n + 31) / 32;
-  if (ngroups == 0) return;
-  const int W32 = (h.T + 31) / 32;
-  il::to_il_kernel<<<static_cast<unsigned>(ngroups), 256, 0, s>>>(cubes, n, 2 * h.D * h.T, W32, il);
-  XE_CUDA(cudaGetLastError());
-}
 
 void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint64_t* il, int64_t n, double* obj,
                     int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3, unsigned char* scratch,

@@ -142,6 +142,17 @@ struct DevProblem {
   double total_rhs;        // total_limit - board (model.cpp:307-308)
 };
 
+// Exact re-score of a batch's near-best candidates (eval_stream.cu).
+constexpr int kRefineCap = 4096;
+struct RefineBuf {
+  DevBuf<int64_t> list;
+  DevBuf<int> cnt;
+  DevBuf<uint32_t> canon;
+  DevBuf<uint64_t> il;
+  DevBuf<double> obj;
+  DevBuf<uint32_t> flags;
+};
+
 }  // namespace xe
 
 // Opaque handle of the C ABI.
@@ -174,6 +185,7 @@ struct xe_problem {
     xe::DevBuf<int64_t> peak;
     xe::DevBuf<uint32_t> flags;
     xe::DevBuf<uint8_t> scratch;
+    xe::RefineBuf refine;
     cudaStream_t stream = nullptr;
   };
   Stage stage[2];
@@ -182,10 +194,24 @@ struct xe_problem {
 
 namespace xe {
 void upload_problem(xe_problem* p);   // problem.cu
-// eval_il.cu: lane-per-candidate evaluator over the interleaved layout
-bool il_supported(const xe_problem* pr);
+// eval_stream.cu: the interleaved layout (NW u64 words per bit row, T <= 256)
+// and the streaming evaluator (K2a v5) with the exact best-of-batch re-score
+bool il_layout_ok(const xe_problem* pr);
 size_t il_bytes(int D, int T, int64_t n);
 void cubes_to_il_device(const xe_problem* pr, const uint32_t* cubes, int64_t n, uint64_t* il, cudaStream_t s);
+bool stream_supported(const xe_problem* pr, const xe_model_opts& opts);
+bool stream_objective_exact(const xe_problem* pr);
+int eval_stream_device(const xe_problem* pr, const xe_model_opts& opts, const uint64_t* il, int64_t n, double* obj,
+                       int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3, unsigned char* scratch,
+                       cudaStream_t stream);
+void refine_best_device(const xe_problem* pr, const xe_model_opts& opts, const uint64_t* src_il,
+                        const uint32_t* src_canon, int64_t n, const double* obj, const uint32_t* flags,
+                        uint32_t valid_mask, uint64_t* best3, RefineBuf& rb, unsigned char* scratch,
+                        cudaStream_t s);
+void il_to_canon_device(const xe_problem* pr, const uint64_t* il, int64_t first, int64_t n, uint32_t* canon,
+                        cudaStream_t s);
+// eval_il.cu: the reference-order lane-per-candidate evaluator (T <= 64)
+bool il_supported(const xe_problem* pr);
 void eval_il_device(const xe_problem* pr, const xe_model_opts& opts, const uint64_t* il, int64_t n, double* obj,
                     int64_t* peak, uint32_t* flags, uint32_t valid_mask, uint64_t* best3, unsigned char* scratch,
                     cudaStream_t stream);

@@ -1,7 +1,11 @@
 # SPDX-License-Identifier: Apache-2.0
 """K2a parity on the GPU: the sm_100a evaluator against the reference's
-golden vectors (bit-exact objective bits, peaks, flags) and against the CPU
-oracle on fresh seeded candidates for every config shape."""
+golden vectors and against the CPU oracle on fresh seeded candidates for
+every config shape.  Peaks and flags bit-exact; per-candidate objectives
+bit-exact when the problem's terms are dyadic (Problem.objective_order_exact)
+and otherwise within REL of the reference's sequential sum (the streaming
+kernel sums per timestep; north_star tolerance 1e-6); the best-of-batch
+objective and index always bit-exact (the exact re-score)."""
 import numpy as np
 import pytest
 
@@ -32,9 +36,16 @@ def run_gpu(problem, cubes, strict=False, energy=False):
     return (r.obj.cpu().numpy(), r.peak.cpu().numpy(), r.flags.cpu().numpy().view(np.uint32), r)
 
 
-def compare(o, p, f, ro, rp, rf):
-    assert np.array_equal(o.view(np.int64), ro.view(np.int64)), \
-        f"objective bits differ at {np.nonzero(o.view(np.int64) != ro.view(np.int64))[0][:5]}"
+REL = 1e-12  # per-candidate objective tolerance when the order is not exact
+
+
+def compare(o, p, f, ro, rp, rf, exact=True):
+    if exact:
+        assert np.array_equal(o.view(np.int64), ro.view(np.int64)), \
+            f"objective bits differ at {np.nonzero(o.view(np.int64) != ro.view(np.int64))[0][:5]}"
+    else:
+        err = np.abs(o - ro) / np.maximum(np.abs(ro), 1e-300)
+        assert np.all(err <= REL), f"objective off by {err.max():.3g} at {np.argmax(err)}"
     assert np.array_equal(p, rp), f"peaks differ at {np.nonzero((p != rp).any(1))[0][:5]}"
     mask = 0xFFFF | _lib.F_DECODE
     bad = np.nonzero((f & mask) != (rf & mask))[0]
@@ -49,8 +60,24 @@ def test_eval_vs_reference_golden(name):
     prob = xe.Problem.from_json(doc(name))
     for strict in (0, 1):
         for en in ((0, 1) if name == "fig2_energy" else (0,)):
-            o, p, f, _ = run_gpu(prob, z["cubes"], strict, en)
-            compare(o, p, f, z[f"obj_s{strict}e{en}"], z[f"peak_s{strict}e{en}"], z[f"flags_s{strict}e{en}"])
+            o, p, f, r = run_gpu(prob, z["cubes"], strict, en)
+            ro, rf = z[f"obj_s{strict}e{en}"], z[f"flags_s{strict}e{en}"]
+            compare(o, p, f, ro, z[f"peak_s{strict}e{en}"], rf, exact=prob.objective_order_exact or en)
+            check_best(r, ro, rf)
+
+
+def check_best(r, ro, rf, mask=_lib.F_CHECK_MASK):
+    """best-of-batch = the reference's first minimum, same objective bits"""
+    valid = (rf & mask) == 0
+    assert r.n_valid == int(valid.sum())
+    if not valid.any():
+        assert r.best_index == -1
+        return
+    idx = np.nonzero(valid)[0]
+    keys = ro[idx].view(np.int64)
+    best = idx[np.argmin(keys)]
+    assert r.best_index == best, (r.best_index, best)
+    assert np.float64(r.best_obj).view(np.int64) == ro[best].view(np.int64)
 
 
 @pytest.mark.parametrize("name,n", [("fig2", 3000), ("vgg16", 400), ("resnet50", 40), ("unet", 30),
@@ -61,9 +88,10 @@ def test_eval_vs_oracle_fresh(oracle, name, n):
     prob = xe.Problem.from_json(text)
     cubes = cubegen.mixed_cubes(a, n, seed=99, random_frac=0.02)
     for strict in (0, 1):
-        o, p, f, _ = run_gpu(prob, cubes, strict)
+        o, p, f, r = run_gpu(prob, cubes, strict)
         ro, rp, rf = oracle.eval_cubes(a, cubes, strict)
-        compare(o, p, f, ro, rp, rf)
+        compare(o, p, f, ro, rp, rf, exact=prob.objective_order_exact)
+        check_best(r, ro, rf)
 
 
 def test_best_of_batch_and_host_path(oracle):
@@ -72,11 +100,10 @@ def test_best_of_batch_and_host_path(oracle):
     prob = xe.Problem.from_json(text)
     cubes = cubegen.mixed_cubes(a, 2000, seed=5, random_frac=0.0)
     o, p, f, r = run_gpu(prob, cubes)
+    ro, rp, rf = oracle.eval_cubes(a, cubes)
     valid = (f & _lib.F_CHECK_MASK) == 0
     assert r.n_valid == int(valid.sum()) > 0
-    idx = np.nonzero(valid)[0]
-    best = idx[np.argmin(o[idx])]          # first minimum (solver.cpp:57-61 rule)
-    assert r.best_index == best and r.best_obj == o[best]
+    check_best(r, ro, rf)                  # first minimum (solver.cpp:57-61 rule), exact bits
     h = xe.evaluate_cubes_host(prob, cubes)
     assert np.array_equal(h.obj.view(np.int64), o.view(np.int64))
     assert np.array_equal(h.peak, p) and np.array_equal(h.flags, f)
@@ -95,26 +122,28 @@ def test_unaligned_and_odd_sizes(oracle):
     prob = xe.Problem.from_json(text)
     for n in (1, 15, 17, 33, 1000):
         cubes = cubegen.mixed_cubes(a, n, seed=n)
-        o, p, f, _ = run_gpu(prob, cubes)
+        o, p, f, r = run_gpu(prob, cubes)
         ro, rp, rf = oracle.eval_cubes(a, cubes)
         compare(o, p, f, ro, rp, rf)
+        check_best(r, ro, rf)
     t = torch.zeros((0, prob.cube_words), dtype=torch.int32, device="cuda")
     r = xe.evaluate_cubes(prob, t)
     assert r.best_index == -1 and r.n_valid == 0
 
 
-@pytest.mark.parametrize("name", ["fig2", "vgg16", "rand3", "chain3"])
+@pytest.mark.parametrize("name", ["fig2", "vgg16", "rand3", "chain3", "resnet50", "unet"])
 def test_interleaved_layout_matches_canonical(oracle, name):
     """xe_cube_il (lane-per-candidate kernel fed directly) == the canonical
     entry point == the CPU oracle, including a ragged last group."""
     text = doc(name)
     a = xo.arrays_from_json(text)
     prob = xe.Problem.from_json(text)
-    n = 1000 + 13
+    n = 1000 + 13 if prob.T <= 64 else 64 + 13
     cubes = cubegen.mixed_cubes(a, n, seed=7, random_frac=0.05)
     t = torch.from_numpy(cubes.view(np.int32)).cuda()
     il = xe.cubes_to_il(prob, t)
-    assert il.numel() * 8 == ((n + 31) // 32) * 32 * 2 * prob.D * prob.T * 8
+    nw = (prob.T + 63) // 64
+    assert il.numel() * 8 == ((n + 31) // 32) * 32 * 2 * prob.D * prob.T * nw * 8
     for strict in (0, 1):
         opts = xe.ModelOptions(strict_free=bool(strict))
         r = xe.evaluate_cubes_il(prob, il, n, opts)
@@ -124,5 +153,7 @@ def test_interleaved_layout_matches_canonical(oracle, name):
         assert np.array_equal(r.peak.cpu().numpy(), p)
         assert np.array_equal(r.flags.cpu().numpy().view(np.uint32), f)
         assert (r.best_index, r.n_valid) == (rc.best_index, rc.n_valid)
+        assert np.float64(r.best_obj).view(np.int64) == np.float64(rc.best_obj).view(np.int64)
         ro, rp, rf = oracle.eval_cubes(a, cubes, strict)
-        compare(o, p, f, ro, rp, rf)
+        compare(o, p, f, ro, rp, rf, exact=prob.objective_order_exact)
+        check_best(r, ro, rf)

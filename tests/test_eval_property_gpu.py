@@ -2,8 +2,8 @@
 """Property sweep of the K2a evaluators against the CPU oracle (pinned to the
 reference, tests/test_oracle_cpu.py) on random problems outside the fixture
 shapes: T up to 64 (interleaved one-word kernel) and up to 140 (warp kernel),
-D in 1..8 (every MAXD instantiation), non-dyadic costs (the sequential fp64
-path), per-edge copy overrides, dst-unsorted edge orders (the ordered copy
+D in 1..8 (every MAXD instantiation), non-dyadic costs (per-candidate objectives
+within 1e-12 relative, the best-of-batch bit-exact), per-edge copy overrides, dst-unsorted edge orders (the ordered copy
 walk), tight budgets (BUDGET / U_BOUND flags), strict and default hazards,
 and an energy section.  Bit-exact objectives, peaks and flags."""
 import json
@@ -74,7 +74,15 @@ def test_random_problems_vs_oracle(oracle, seed, T, D):
                 torch.cuda.synchronize()
                 o, p, f = r.obj.cpu().numpy(), r.peak.cpu().numpy(), r.flags.cpu().numpy().view(np.uint32)
                 ro, rp, rf = oracle.eval_cubes(a, cubes, strict, energy)
-                assert np.array_equal(o.view(np.int64), ro.view(np.int64)), (seed, strict, energy, sort_by_dst)
+                if energy or prob.objective_order_exact:
+                    assert np.array_equal(o.view(np.int64), ro.view(np.int64)), (seed, strict, energy, sort_by_dst)
+                else:  # per-timestep reassociation (test_eval_gpu.REL)
+                    assert np.all(np.abs(o - ro) <= 1e-12 * np.abs(ro)), (seed, strict, sort_by_dst)
+                valid = (rf & _lib.F_CHECK_MASK) == 0
+                if valid.any():
+                    idx = np.nonzero(valid)[0]
+                    best = idx[np.argmin(ro[idx].view(np.int64))]
+                    assert r.best_index == best and np.float64(r.best_obj).view(np.int64) == ro[best].view(np.int64)
                 assert np.array_equal(p, rp)
                 mask = 0xFFFF | _lib.F_DECODE
                 assert np.array_equal(f & mask, rf & mask)
