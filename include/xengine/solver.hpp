@@ -3,10 +3,13 @@
 // Placement solvers (drop-in for proj/include/xengine/solver.hpp:13-40).
 //   save_all_assignment  save-all (R, S) cubes of a placement, completed on the GPU
 //   assignment_oracle    the full D^T placement sweep as one GPU launch (K2b)
-//   solve_search         the GPU best-schedule search (xe_search), in place of
-//                        solve_exact / solve_external (solver.hpp:42-58)
-// solve_exact / solve_external themselves (memoised DFS, MPS file bridge) are
-// outside the B200 hot path.
+//   solve_exact          the reference's exact search (solver.cpp:101-489) as a
+//                        GPU dynamic program over the same states (xe_solve_exact):
+//                        same optimum, same tail_less tie-break, same statuses
+//   solve_search         the GPU best-schedule search for problems beyond
+//                        solve_exact's D*T <= 64 (xe_search)
+// solve_external (the MPS file bridge to an external MILP solver) is outside
+// the B200 hot path.
 #pragma once
 
 #include <cstdint>
@@ -37,6 +40,17 @@ struct Solution {
 
 Assignment save_all_assignment(const Problem& p, const std::vector<int>& devices);
 Solution assignment_oracle(const Problem& p);
+
+// Memoized search over (timestep, per-device saved set) states (solver.hpp:42-50):
+// per timestep the new operator on one device, optional recomputations of
+// earlier operators that feed a computation of this timestep, any saved
+// subset with a future consumer; memory trajectory within budget.  Proves
+// optimality or infeasibility when it runs to completion; D*T <= 64
+// (TooLarge otherwise).  Empty budgets means the problem's device budgets.
+// Here: the same state space expanded level by level on the GPU; nodes_explored
+// counts the legal (state, computation set) frames.
+Solution solve_exact(const Problem& p, const ModelOptions& opts = {}, std::vector<std::int64_t> budgets = {},
+                     const SearchLimits& limits = {});
 
 // Parameters of solve_search (xe_search_opts in include/xengine_b200.h).
 struct SearchParams {

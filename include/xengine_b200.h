@@ -143,6 +143,10 @@ int xe_problem_create(const xe_problem_desc* desc, int device, xe_problem** out)
 int xe_problem_destroy(xe_problem* p);
 /* Host view of the resolved arrays (pointers stay valid for the handle's life). */
 int xe_problem_describe(const xe_problem* p, xe_problem_desc* out);
+/* Names of the loaded document (synthesized "d<k>" / "op<i>" for handles built
+ * from arrays); NULL for an out-of-range index. */
+const char* xe_problem_device_id(const xe_problem* p, int32_t d);
+const char* xe_problem_op_name(const xe_problem* p, int32_t i);
 /* with_budgets (problem.cpp:382-393): new handle, same problem, new budgets. */
 int xe_problem_with_budgets(const xe_problem* p, const int64_t* budgets, xe_problem** out);
 
@@ -224,6 +228,10 @@ size_t xe_cube_bytes(int32_t D, int32_t T);
  * are always exact: the near-best candidates are re-scored in the
  * reference's order and the first minimum of those bits wins. */
 int xe_objective_order_exact(const struct xe_problem* p, int32_t* exact);
+/* Per handle: exact != 0 makes every batched evaluation sum each candidate's
+ * objective in the reference's order (the reference-order kernels; slower),
+ * 0 (default) allows the streaming evaluator's reassociation. */
+int xe_problem_set_exact_objective(struct xe_problem* p, int32_t exact);
 
 typedef struct xe_eval_out {
   double* obj;      /* [n] objective_value of the completion (model.cpp:369-428), see above */
@@ -383,11 +391,15 @@ typedef struct xe_search_result {
                                  the local search reached feasibility from over-budget candidates) */
   double rounding_objective;  /* best rounding candidate alone */
   int64_t index;              /* its global index (-1: no valid candidate) */
-  double lp_bound;            /* LP relaxation value (NaN without LP) */
+  double lp_bound;            /* valid lower bound from the LP duals (NaN without LP; -inf when the
+                                 prohibitive-cost presolve is not certified by the duals) */
   int32_t has_lp, lp_certified;
   int64_t n_evaluated, n_valid; /* candidates scored; valid rounding candidates */
   int32_t improvements;       /* local-search improvements of the incumbent */
   int32_t time_limited;       /* 1: the time limit cut the search short */
+  double lp_value;            /* PDHG primal objective (the relaxation's value to the tolerance) */
+  int32_t lp_converged;       /* 1: PDHG met its tolerance (0: iteration limit) */
+  int32_t pad_;
 } xe_search_result;
 
 void xe_search_opts_default(xe_search_opts* o);
@@ -395,6 +407,106 @@ void xe_search_opts_default(xe_search_opts* o);
  * NULL; peaks_host: [D] its per-device peaks, or NULL. */
 int xe_search(const xe_problem* p, const xe_model_opts* opts, const xe_search_opts* so, xe_search_result* res,
               uint32_t* cube_host, int64_t* peaks_host, void* stream);
+
+/* ---- solve_exact (proj/include/xengine/solver.hpp:42-50) -------------------
+ * The reference's exact search (proj/src/solver.cpp:101-489: per timestep the
+ * new operator on one device, recomputations feeding this timestep's
+ * computations, saves of tensors with a later consumer, memory trajectory
+ * within budget; optimum under tail_less = (cost, sum R, sum S, bit string),
+ * solver.cpp:87-92) as a level-synchronous GPU dynamic program over the same
+ * (timestep, saved-set) states.  Requires D*T <= 64 like the reference
+ * (XE_ERR_TOO_LARGE otherwise).  Budgets: the handle's (use
+ * xe_problem_with_budgets for solve_exact's budget override). */
+typedef struct xe_exact_opts {
+  int64_t node_limit;     /* SearchLimits::node_limit (< 0: none); nodes = legal
+                             (state, computation set) frames expanded */
+  int64_t time_limit_ms;  /* SearchLimits::time_limit_ms (< 0: none), checked between launches */
+  double upper_bound;     /* search-space cost of a known schedule (prunes; INFINITY: none) */
+  int64_t max_states;     /* per timestep (default 1 << 26); beyond it: LimitReached */
+} xe_exact_opts;
+
+typedef struct xe_exact_result {
+  int32_t status;         /* 0 Optimal, 1 Infeasible, 2 LimitReached (SolveStatus order) */
+  int32_t found;          /* 1: cube_host holds the optimal schedule */
+  double objective;       /* the search's tail cost (solver.cpp:284, reported as objective_ms); NaN if none */
+  int64_t sum_r, sum_s;   /* tail_less keys of the optimum */
+  int64_t nodes, states;  /* frames expanded, distinct states kept */
+  double ms;              /* wall clock */
+} xe_exact_result;
+
+void xe_exact_opts_default(xe_exact_opts* o);
+/* cube_host: [xe_cube_bytes(D, T) / 4] canonical (R, S) cube of the optimum
+ * (R(d,t,.) = the computation set of t, S(d,t+1,.) = the exit set of t,
+ * solver.cpp:426-437), or NULL. */
+int xe_solve_exact(const xe_problem* p, const xe_model_opts* opts, const xe_exact_opts* eo,
+                   xe_exact_result* res, uint32_t* cube_host, void* stream);
+
+/* ---- schedules: decode / validate / replay (proj/src/schedule.cpp) -------
+ * proj/include/xengine/schedule.hpp:15-126.  The executable reading of a
+ * schedule, computed on the GPU for a batch (the top-K of an evaluated set):
+ * per timestep copies (source: lowest device holding the tensor), the
+ * compute, the fired frees, then end-of-timestep drops. */
+typedef struct xe_action {
+  int32_t kind;  /* ActionKind: 0 Compute, 1 Copy, 2 Free, 3 Drop */
+  int32_t timestep, slot;
+  int32_t device, op;   /* Compute / Free / Drop (op: Compute / Drop) */
+  int32_t src, dst;     /* Copy / Free: edge endpoints (src == dst: a self edge) */
+  int32_t from, to;     /* Copy: devices */
+} xe_action;
+
+typedef struct xe_decode_error {
+  int32_t code;  /* 0 ok; IllegalAssignment: 1 tensor u resident on no device,
+                    2 the copy source of u was freed earlier in timestep t (schedule.cpp:57-71) */
+  int32_t t, v, u;
+} xe_decode_error;
+
+/* decode(complete_assignment(R, S)) of n canonical cubes (host): actions of
+ * candidate k in actions[offsets[k] .. offsets[k+1]) (empty when errors[k].code
+ * != 0).  actions == NULL: offsets only (size the buffer, call again). */
+int xe_decode_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes, int64_t n,
+                    int64_t* offsets /* [n+1] */, xe_action* actions, xe_decode_error* errors /* [n] or NULL */);
+/* decode of one dense assignment x[n_cols] (VarRef order): R, Z, S, F bits are
+ * the assignment's own values > 0.5, as decode reads the map (schedule.cpp:40-129). */
+int xe_decode_dense(const xe_problem* p, const double* x, int64_t* n_actions, xe_action* actions,
+                    xe_decode_error* error);
+
+typedef struct xe_violation {
+  int32_t kind;   /* ViolationKind: 0 ComputeWithoutInputs, 1 CopyFromNonResident,
+                     2 BudgetExceeded, 3 FreeNonResident, 4 UncomputedOperator */
+  int32_t device, timestep, slot;
+  int64_t bytes;  /* BudgetExceeded: occupied bytes at the check */
+  int32_t a, b;   /* detail operands: (operator, missing input) | tensor | operator */
+} xe_violation;
+
+/* validate (schedule.cpp:131-240) of n action lists (host arrays as from
+ * xe_decode_cubes); budgets [D] or NULL (the problem's).  violations == NULL:
+ * v_offsets only. */
+int xe_validate_schedules(const xe_problem* p, const xe_action* actions, const int64_t* offsets, int64_t n,
+                          const int64_t* budgets, int64_t* v_offsets /* [n+1] */, xe_violation* violations);
+/* replay (schedule.cpp:261-369) of n LEGAL action lists (run validate first:
+ * the reference raises IllegalSchedule): total action cost (NaN when a copy
+ * runs along an undeclared edge: the caller prices it with the link model),
+ * the Eq. 1 objective rebuilt from availability, the per-slot memory series
+ * memory[n][D][T][T] (or NULL) and the per-device peaks [n][D]. */
+int xe_replay_schedules(const xe_problem* p, const xe_model_opts* opts, const xe_action* actions,
+                        const int64_t* offsets, int64_t n, double* total_ms, double* eq1, int64_t* memory,
+                        int64_t* peaks);
+/* Text forms (host): format_schedule (schedule.cpp:440-475) and trace_csv
+ * (:523-530) with the problem's device ids and operator names.  buf NULL:
+ * *len = bytes needed. */
+int xe_format_schedule(const xe_problem* p, const xe_action* actions, int64_t n_actions, char* buf, size_t* len);
+int xe_trace_csv(const xe_problem* p, const int64_t* memory /* [D][T][T] */, char* buf, size_t* len);
+/* parse_schedule (schedule.cpp:477-521): *n_actions in/out (capacity / count). */
+int xe_parse_schedule(const xe_problem* p, const char* text, xe_action* actions, int64_t* n_actions);
+/* The same with caller-provided names (device_ids [D], op_names [T], the
+ * problem name for parse errors; NULL: the handle's). */
+int xe_format_schedule_named(const xe_problem* p, const xe_action* actions, int64_t n_actions,
+                             const char* const* device_ids, const char* const* op_names, char* buf, size_t* len);
+int xe_trace_csv_named(const xe_problem* p, const int64_t* memory, const char* const* device_ids, char* buf,
+                       size_t* len);
+int xe_parse_schedule_named(const xe_problem* p, const char* text, const char* const* device_ids,
+                            const char* const* op_names, const char* problem_name, xe_action* actions,
+                            int64_t* n_actions);
 
 #ifdef __cplusplus
 }

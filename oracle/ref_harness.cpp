@@ -12,6 +12,8 @@
 //   objective_value         proj/src/model.cpp:369-428
 //   check_assignment        proj/src/model.cpp:430-469
 //   decode                  proj/src/schedule.cpp:40-129
+//   validate / replay       proj/src/schedule.cpp:131-369
+//   format_schedule / parse_schedule / trace_csv  proj/src/schedule.cpp:440-530
 //   save_all_assignment     proj/src/solver.cpp:30-42
 //   assignment_oracle       proj/src/solver.cpp:44-75
 //   solve_exact             proj/src/solver.cpp:449-489
@@ -463,6 +465,79 @@ int64_t xr_budget_percent(int64_t full, double pct, int* rc) {
   } catch (const Error& e) {
     *rc = fail(e);
     return 0;
+  }
+}
+
+namespace {
+char* dup_out(const std::string& s, size_t* len) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.data(), s.size());
+  p[s.size()] = 0;
+  *len = s.size();
+  return p;
+}
+}  // namespace
+
+// decode(complete_assignment(R,S)) -> format_schedule; replay with the
+// assignment -> trace_csv, total_action_ms, eq1_objective_ms, peaks
+int xr_schedule(void* hv, int strict, int energy, const uint32_t* cube, char** text, size_t* tlen,
+                char** csv, size_t* clen, double* total_ms, double* eq1, int64_t* peaks) {
+  auto* h = static_cast<Handle*>(hv);
+  try {
+    ModelOptions opts = make_opts(h, strict, 0, energy);
+    const int D = h->p.device_count(), T = h->p.op_count();
+    BitCube R(D, T), S(D, T);
+    unpack(cube, D, T, R, S);
+    Assignment a = complete_assignment(h->p, opts, R, S);
+    Schedule sc = decode(a, h->p);
+    *text = dup_out(format_schedule(sc), tlen);
+    Trace tr = replay(sc, h->p, opts, a);
+    *csv = dup_out(trace_csv(tr, h->p), clen);
+    *total_ms = tr.total_action_ms;
+    *eq1 = tr.eq1_objective_ms;
+    for (int d = 0; d < D; ++d) peaks[d] = tr.peaks[static_cast<size_t>(d)];
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+// validate(parse_schedule(text)) -> one line per violation:
+// "<kind> <device> <timestep> <slot> <bytes>|<detail>"
+int xr_validate_text(void* hv, const char* text, const int64_t* budgets, char** out, size_t* len) {
+  auto* h = static_cast<Handle*>(hv);
+  try {
+    Schedule sc = parse_schedule(text, h->p);
+    std::vector<int64_t> b;
+    if (budgets) b.assign(budgets, budgets + h->p.device_count());
+    ValidationReport rep = validate(sc, h->p, b);
+    std::string o;
+    for (const auto& v : rep.violations)
+      o += std::string(violation_name(v.kind)) + " " + std::to_string(v.device) + " " + std::to_string(v.timestep) +
+           " " + std::to_string(v.slot) + " " + std::to_string(v.bytes) + "|" + v.detail + "\n";
+    *out = dup_out(o, len);
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
+  }
+}
+
+// replay(parse_schedule(text)) without an assignment (availability rebuilt
+// from the actions) -> trace_csv, totals, peaks
+int xr_replay_text(void* hv, int strict, int energy, const char* text, char** csv, size_t* clen,
+                   double* total_ms, double* eq1, int64_t* peaks) {
+  auto* h = static_cast<Handle*>(hv);
+  try {
+    ModelOptions opts = make_opts(h, strict, 0, energy);
+    Schedule sc = parse_schedule(text, h->p);
+    Trace tr = replay(sc, h->p, opts);
+    *csv = dup_out(trace_csv(tr, h->p), clen);
+    *total_ms = tr.total_action_ms;
+    *eq1 = tr.eq1_objective_ms;
+    for (int d = 0; d < h->p.device_count(); ++d) peaks[d] = tr.peaks[static_cast<size_t>(d)];
+    return 0;
+  } catch (const Error& e) {
+    return fail(e);
   }
 }
 

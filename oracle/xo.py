@@ -647,6 +647,10 @@ class Ref:
         L.xr_budget_percent.argtypes = [C.c_int64, C.c_double, C.c_void_p]
         L.xr_budget_percent.restype = C.c_int64
         L.xr_free.argtypes = [C.c_void_p]
+        sp = [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
+        L.xr_schedule.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p] + sp + sp + [C.c_void_p] * 3
+        L.xr_validate_text.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p] + sp
+        L.xr_replay_text.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p] + sp + [C.c_void_p] * 3
 
     def _check(self, rc):
         if rc != 0:
@@ -773,6 +777,37 @@ class RefProblem:
         self.ref._check(self.L.xr_assignment_oracle(self.h, C.byref(obj), dev.ctypes.data,
                                                     C.byref(nodes)))
         return obj.value, dev, nodes.value
+
+    def _take(self, p, n):
+        b = C.string_at(p, n.value).decode()
+        self.L.xr_free(p)
+        return b
+
+    def schedule(self, cube, D, strict=False, energy=False):
+        """decode -> format_schedule, replay(assignment) -> trace_csv,
+        total_action_ms, eq1_objective_ms, peaks (schedule.cpp:40-530)."""
+        t, tl, c, cl = C.c_void_p(), C.c_size_t(), C.c_void_p(), C.c_size_t()
+        tot, eq1 = C.c_double(), C.c_double()
+        peaks = np.zeros(D, np.int64)
+        cube = np.ascontiguousarray(cube, np.uint32)
+        self.ref._check(self.L.xr_schedule(self.h, int(strict), int(energy), cube.ctypes.data, C.byref(t), C.byref(tl),
+                                           C.byref(c), C.byref(cl), C.byref(tot), C.byref(eq1), peaks.ctypes.data))
+        return self._take(t, tl), self._take(c, cl), tot.value, eq1.value, peaks
+
+    def validate_text(self, text, budgets=None):
+        """validate(parse_schedule(text)) -> ["kind device t slot bytes|detail", ...]"""
+        o, ol = C.c_void_p(), C.c_size_t()
+        b = None if budgets is None else np.ascontiguousarray(budgets, np.int64)
+        self.ref._check(self.L.xr_validate_text(self.h, text.encode(), None if b is None else b.ctypes.data,
+                                                C.byref(o), C.byref(ol)))
+        return [x for x in self._take(o, ol).split("\n") if x]
+
+    def replay_text(self, text, D, strict=False, energy=False):
+        c, cl, tot, eq1 = C.c_void_p(), C.c_size_t(), C.c_double(), C.c_double()
+        peaks = np.zeros(D, np.int64)
+        self.ref._check(self.L.xr_replay_text(self.h, int(strict), int(energy), text.encode(), C.byref(c),
+                                              C.byref(cl), C.byref(tot), C.byref(eq1), peaks.ctypes.data))
+        return self._take(c, cl), tot.value, eq1.value, peaks
 
     def solve_exact(self, D, T, strict=False, energy=False, budgets=None, node_limit=0):
         st, obj, nodes = C.c_int(), C.c_double(), C.c_int64()

@@ -125,7 +125,34 @@ class SearchResult(C.Structure):
     _fields_ = [("objective", C.c_double), ("rounding_objective", C.c_double), ("index", C.c_int64),
                 ("lp_bound", C.c_double), ("has_lp", C.c_int32), ("lp_certified", C.c_int32),
                 ("n_evaluated", C.c_int64), ("n_valid", C.c_int64), ("improvements", C.c_int32),
-                ("time_limited", C.c_int32)]
+                ("time_limited", C.c_int32), ("lp_value", C.c_double), ("lp_converged", C.c_int32),
+                ("pad_", C.c_int32)]
+
+
+class ExactOpts(C.Structure):
+    _fields_ = [("node_limit", C.c_int64), ("time_limit_ms", C.c_int64), ("upper_bound", C.c_double),
+                ("max_states", C.c_int64)]
+
+
+class ExactResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("found", C.c_int32), ("objective", C.c_double),
+                ("sum_r", C.c_int64), ("sum_s", C.c_int64), ("nodes", C.c_int64), ("states", C.c_int64),
+                ("ms", C.c_double)]
+
+
+class Action(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("timestep", C.c_int32), ("slot", C.c_int32), ("device", C.c_int32),
+                ("op", C.c_int32), ("src", C.c_int32), ("dst", C.c_int32), ("from_", C.c_int32),
+                ("to", C.c_int32)]
+
+
+class DecodeError(C.Structure):
+    _fields_ = [("code", C.c_int32), ("t", C.c_int32), ("v", C.c_int32), ("u", C.c_int32)]
+
+
+class Violation(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("device", C.c_int32), ("timestep", C.c_int32), ("slot", C.c_int32),
+                ("bytes", C.c_int64), ("a", C.c_int32), ("b", C.c_int32)]
 
 
 # symbol -> (restype, argtypes); the set of exports include/xengine_b200.h declares
@@ -154,6 +181,9 @@ SIGNATURES = {
                                      C.c_uint32, C.POINTER(Best)]),
     "xe_cube_il_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int64]),
     "xe_objective_order_exact": (C.c_int, [P, C.POINTER(C.c_int32)]),
+    "xe_problem_set_exact_objective": (C.c_int, [P, C.c_int32]),
+    "xe_problem_device_id": (C.c_char_p, [P, C.c_int32]),
+    "xe_problem_op_name": (C.c_char_p, [P, C.c_int32]),
     "xe_cubes_to_il": (C.c_int, [P, P, C.c_int64, P, P]),
     "xe_eval_cubes_il": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, C.POINTER(EvalOut),
                                    C.c_uint32, C.POINTER(Best), P]),
@@ -175,6 +205,18 @@ SIGNATURES = {
     "xe_random_placements": (C.c_int, [P, C.c_uint64, C.c_int64, C.c_int64, P, P]),
     "xe_round_cubes": (C.c_int, [P, P, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_double,
                                  P, P]),
+    "xe_exact_opts_default": (None, [C.POINTER(ExactOpts)]),
+    "xe_decode_cubes": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, P, P, P]),
+    "xe_decode_dense": (C.c_int, [P, P, C.POINTER(C.c_int64), P, P]),
+    "xe_validate_schedules": (C.c_int, [P, P, P, C.c_int64, P, P, P]),
+    "xe_replay_schedules": (C.c_int, [P, C.POINTER(ModelOpts), P, P, C.c_int64, P, P, P, P]),
+    "xe_format_schedule": (C.c_int, [P, P, C.c_int64, P, C.POINTER(C.c_size_t)]),
+    "xe_format_schedule_named": (C.c_int, [P, P, C.c_int64, P, P, P, C.POINTER(C.c_size_t)]),
+    "xe_trace_csv": (C.c_int, [P, P, P, C.POINTER(C.c_size_t)]),
+    "xe_trace_csv_named": (C.c_int, [P, P, P, P, C.POINTER(C.c_size_t)]),
+    "xe_parse_schedule": (C.c_int, [P, C.c_char_p, P, C.POINTER(C.c_int64)]),
+    "xe_parse_schedule_named": (C.c_int, [P, C.c_char_p, P, P, C.c_char_p, P, C.POINTER(C.c_int64)]),
+    "xe_solve_exact": (C.c_int, [P, P, C.POINTER(ExactOpts), C.POINTER(ExactResult), P, P]),
 }
 
 
@@ -184,7 +226,10 @@ def load(path: str = LIB_PATH):
             f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
             "(the B200 path has no CPU fallback)")
     lib = C.CDLL(path)
+    lenient = os.environ.get("XE_LIB_LENIENT") == "1"  # A/B runs against older builds
     for name, (res, args) in SIGNATURES.items():
+        if lenient and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

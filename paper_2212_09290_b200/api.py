@@ -148,6 +148,18 @@ class Problem:
         check(LIB.xe_objective_order_exact(self._h, C.byref(x)))
         return bool(x.value)
 
+    def names(self) -> dict:
+        """Device ids and operator names of the document (problem.hpp:18-60)."""
+        return {"devices": [LIB.xe_problem_device_id(self._h, d).decode() for d in range(self.D)],
+                "ops": [LIB.xe_problem_op_name(self._h, i).decode() for i in range(self.T)]}
+
+    def set_exact_objective(self, exact: bool = True) -> "Problem":
+        """Every batched evaluation on this handle sums each candidate's
+        objective in the reference's order (objective_value, model.cpp:
+        392-411) when exact, at the reference-order kernels' speed."""
+        check(LIB.xe_problem_set_exact_objective(self._h, int(bool(exact))))
+        return self
+
 
 @dataclass
 class EvalResult:
@@ -314,6 +326,39 @@ def assignment_oracle(problem: Problem):
     dev = np.zeros(problem.T, np.int32)
     check(LIB.xe_assignment_oracle(problem.handle, C.byref(obj), dev.ctypes.data, C.byref(n)))
     return obj.value, dev, n.value
+
+
+@dataclass
+class ExactResult:
+    status: str                   # "optimal" | "infeasible" | "limit" (status_name, solver.cpp)
+    objective: float              # the search's tail cost (objective_ms); nan without a solution
+    cube: Optional[np.ndarray]    # canonical (R, S) cube words of the optimum (uint32), None without one
+    sum_r: int                    # tail_less keys of the optimum (solver.cpp:87-92)
+    sum_s: int
+    nodes: int                    # legal (state, computation set) frames expanded
+    states: int                   # distinct (timestep, saved-set) states kept
+    ms: float
+
+
+def solve_exact(problem: Problem, opts: Optional[ModelOptions] = None, node_limit: Optional[int] = None,
+                time_limit_ms: Optional[int] = None, upper_bound: float = float("inf")) -> ExactResult:
+    """solve_exact (solver.hpp:42-50, solver.cpp:449-489) as the GPU dynamic
+    program of csrc/exact.cu: same states, transitions and tail_less optimum
+    as the reference's memoised DFS.  Budgets are the problem's (use
+    Problem.with_budgets for the reference's budget override)."""
+    o = _lib.ExactOpts()
+    LIB.xe_exact_opts_default(C.byref(o))
+    if node_limit is not None:
+        o.node_limit = int(node_limit)
+    if time_limit_ms is not None:
+        o.time_limit_ms = int(time_limit_ms)
+    o.upper_bound = float(upper_bound)
+    r = _lib.ExactResult()
+    cube = np.zeros(LIB.xe_cube_bytes(problem.D, problem.T) // 4, np.uint32)
+    mo = (opts or ModelOptions()).c()
+    check(LIB.xe_solve_exact(problem.handle, C.byref(mo), C.byref(o), C.byref(r), cube.ctypes.data, None))
+    status = {0: "optimal", 1: "infeasible", 2: "limit"}[r.status]
+    return ExactResult(status, r.objective, cube if r.found else None, r.sum_r, r.sum_s, r.nodes, r.states, r.ms)
 
 
 class _DevArray:

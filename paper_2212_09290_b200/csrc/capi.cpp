@@ -242,6 +242,16 @@ int xe_problem_destroy(xe_problem* p) {
   });
 }
 
+const char* xe_problem_device_id(const xe_problem* p, int32_t d) {
+  if (!p || d < 0 || d >= p->h.D || static_cast<size_t>(d) >= p->h.device_ids.size()) return nullptr;
+  return p->h.device_ids[static_cast<size_t>(d)].c_str();
+}
+
+const char* xe_problem_op_name(const xe_problem* p, int32_t i) {
+  if (!p || i < 0 || i >= p->h.T || static_cast<size_t>(i) >= p->h.op_names.size()) return nullptr;
+  return p->h.op_names[static_cast<size_t>(i)].c_str();
+}
+
 int xe_problem_describe(const xe_problem* p, xe_problem_desc* o) {
   return guard([&] {
     if (!p || !o) fail(XE_ERR_ARG, "null argument");
@@ -397,7 +407,14 @@ size_t xe_cube_il_bytes(int32_t D, int32_t T, int64_t n) { return il_bytes(D, T,
 int xe_objective_order_exact(const xe_problem* p, int32_t* exact) {
   return guard([&] {
     if (!p || !exact) fail(XE_ERR_ARG, "null argument");
-    *exact = p->device >= 0 && stream_objective_exact(p) ? 1 : 0;
+    *exact = p->device >= 0 && (p->exact_objective || stream_objective_exact(p)) ? 1 : 0;
+  });
+}
+
+int xe_problem_set_exact_objective(xe_problem* p, int32_t exact) {
+  return guard([&] {
+    if (!p) fail(XE_ERR_ARG, "null argument");
+    p->exact_objective = exact != 0;
   });
 }
 

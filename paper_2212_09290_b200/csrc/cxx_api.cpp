@@ -36,6 +36,7 @@
 #include "xengine/mps_io.hpp"
 #include "xengine/model.hpp"
 #include "xengine/problem.hpp"
+#include "xengine/schedule.hpp"
 #include "xengine/solver.hpp"
 #include "xengine_b200.h"
 
@@ -280,13 +281,25 @@ struct DeviceModel {
   }
 };
 
-// Cheap O(rows) identity of a model's row set: a model edited after
-// build_model no longer matches its device copy.
+// O(nnz) identity of everything write_mps / check_assignment read from a
+// model (rows with every term and coefficient, the objective map, quad terms,
+// fixed zeros, budgets): a model edited in place after build_model no longer
+// matches its device copy and is re-uploaded.
 uint64_t fingerprint(const MilpModel& m) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](uint64_t x) {
     h ^= x;
     h *= 1099511628211ull;
+  };
+  auto bits = [](double x) {
+    uint64_t r;
+    std::memcpy(&r, &x, 8);
+    return r;
+  };
+  auto ref = [&](const VarRef& v) {
+    mix(static_cast<uint64_t>(static_cast<uint16_t>(v.a)) << 48 | static_cast<uint64_t>(static_cast<uint16_t>(v.b)) << 32 |
+        static_cast<uint64_t>(static_cast<uint16_t>(v.c)) << 16 | static_cast<uint64_t>(static_cast<uint16_t>(v.d)));
+    mix(static_cast<uint64_t>(v.family));
   };
   mix(m.constraints.size());
   mix(m.objective.size());
@@ -295,11 +308,24 @@ uint64_t fingerprint(const MilpModel& m) {
   mix(static_cast<uint64_t>(m.options.strict_free) | static_cast<uint64_t>(m.options.quadratic_objective) << 1 |
       static_cast<uint64_t>(m.options.energy.has_value()) << 2);
   for (const auto& c : m.constraints) {
-    uint64_t r;
-    std::memcpy(&r, &c.rhs, 8);
     mix(c.terms.size() ^ (static_cast<uint64_t>(c.tag) << 40) ^ (static_cast<uint64_t>(c.ordinal) << 20) ^
-        (static_cast<uint64_t>(c.rel) << 60) ^ r);
+        (static_cast<uint64_t>(c.rel) << 60));
+    mix(bits(c.rhs));
+    for (const auto& [v, x] : c.terms) {
+      ref(v);
+      mix(bits(x));
+    }
   }
+  for (const auto& [v, x] : m.objective) {
+    ref(v);
+    mix(bits(x));
+  }
+  for (const auto& q : m.quad) {
+    mix(static_cast<uint64_t>(q.t) << 32 ^ static_cast<uint64_t>(q.e));
+    mix(static_cast<uint64_t>(q.d_src) << 32 ^ static_cast<uint64_t>(q.d_cmp));
+    mix(bits(q.w));
+  }
+  for (const auto& v : m.fixed_zero) ref(v);
   for (auto b : m.budgets) mix(static_cast<uint64_t>(b));
   return h;
 }
@@ -892,6 +918,21 @@ Assignment save_all_assignment(const Problem& p, const std::vector<int>& devices
 
 Solution assignment_oracle(const Problem& p) {
   validate_problem(p);
+  // the reference's enumeration guard (solver.cpp:47-49); the GPU sweep
+  // itself goes to 2^40 through xe_assignment_oracle
+  double combos = 1.0;
+  for (int i = 0; i < p.op_count(); ++i) combos *= p.device_count();
+  if (combos > 4.0e6) raise(Errc::TooLarge, "placement family too large to enumerate");
+  if (p.device_count() == 1) {  // a single placement (T may exceed the sweep's 64)
+    Solution s;
+    s.status = SolveStatus::Optimal;
+    s.backend = "oracle";
+    s.assignment = save_all_assignment(p, std::vector<int>(static_cast<size_t>(p.op_count()), 0));
+    s.objective_ms = objective_value(s.assignment, p, {});
+    s.assignment.objective_reported = s.objective_ms;
+    s.nodes_explored = 1;
+    return s;
+  }
   Handle h = upload(describe(p, std::nullopt));
   double best = 0.0;
   std::vector<int32_t> dev(static_cast<size_t>(p.op_count()));
@@ -905,6 +946,54 @@ Solution assignment_oracle(const Problem& p) {
   s.assignment.objective_reported = best;
   s.nodes_explored = n;
   return s;
+}
+
+Solution solve_exact(const Problem& p, const ModelOptions& opts, std::vector<std::int64_t> budgets,
+                     const SearchLimits& limits) {
+  Problem peff = budgets.empty() ? p : with_budgets(p, budgets);
+  validate_problem(peff);
+  const int D = peff.device_count(), T = peff.op_count();
+  if (D * T > 64) raise(Errc::TooLarge, "state space exceeds 64 residency bits");
+  Solution out;
+  out.backend = "exact";
+  out.objective_ms = std::numeric_limits<double>::quiet_NaN();
+  Handle h = upload(describe(peff, opts.energy));
+  const xe_model_opts o = c_opts(opts);
+  xe_exact_opts eo;
+  xe_exact_opts_default(&eo);
+  if (limits.node_limit) eo.node_limit = *limits.node_limit;
+  if (limits.time_limit_ms) eo.time_limit_ms = *limits.time_limit_ms;
+  xe_exact_result r{};
+  std::vector<uint32_t> cube(xe_cube_bytes(D, T) / 4);
+  ck(xe_solve_exact(h.get(), &o, &eo, &r, cube.data(), nullptr));
+  out.nodes_explored = r.nodes;
+  if (r.status == 1) {
+    out.status = SolveStatus::Infeasible;
+    return out;
+  }
+  if (!r.found) {
+    out.status = SolveStatus::LimitReached;
+    return out;
+  }
+  // LimitReached keeps the best schedule found so far (solver.cpp:474-478)
+  out.status = r.status == 0 ? SolveStatus::Optimal : SolveStatus::LimitReached;
+  BitCube R(D, T), S(D, T);
+  const int W = (T + 31) / 32;
+  for (int which = 0; which < 2; ++which)
+    for (int d = 0; d < D; ++d)
+      for (int t = 0; t < T; ++t)
+        for (int i = 0; i < T; ++i)
+          if ((cube[((static_cast<size_t>(which) * D + d) * T + t) * W + i / 32] >> (i % 32)) & 1u)
+            (which ? S : R).at(d, t, i) = 1;
+  // fill_solution (solver.cpp:426-446): the search cost must be the
+  // completed assignment's objective
+  out.assignment = complete_assignment(peff, opts, R, S);
+  const double obj = objective_value(out.assignment, peff, opts);
+  if (std::abs(obj - r.objective) > 1e-9 * std::max(1.0, std::abs(obj)))
+    raise(Errc::ObjectiveMismatch, "search cost " + format_number(r.objective) + " vs objective " + format_number(obj));
+  out.objective_ms = r.objective;
+  out.assignment.objective_reported = r.objective;
+  return out;
 }
 
 Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchParams& params) {
@@ -937,9 +1026,11 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
     s.objective_ms = std::numeric_limits<double>::quiet_NaN();
     return s;
   }
-  // the LP value carries the PDHG tolerance (xe_search_opts.lp_tol, 1e-6
-  // relative): the schedule is optimal to that tolerance when it meets it
-  const bool proven = r.has_lp && r.objective <= r.lp_bound + so.lp_tol * std::max(1.0, std::fabs(r.objective));
+  // Optimal only against a certified lower bound (the LP duals' Lagrangian
+  // value, valid for any PDHG iterate): the schedule is optimal to the
+  // relative gap lp_tol (the MILP solvers' mip-gap convention) when it meets it
+  const bool proven = r.has_lp && r.lp_certified && std::isfinite(r.lp_bound) &&
+                      r.objective <= r.lp_bound + so.lp_tol * std::max(1.0, std::fabs(r.objective));
   s.status = proven ? SolveStatus::Optimal : SolveStatus::LimitReached;
   s.objective_ms = r.objective;
   BitCube R(D, T), S(D, T);
@@ -953,6 +1044,252 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
   s.assignment = complete_assignment(p, opts, R, S);
   s.assignment.objective_reported = r.objective;
   return s;
+}
+
+// ============================ schedule.hpp =================================
+// decode / validate / replay on the GPU (csrc/schedule.cu), text forms by the
+// library's one writer (csrc/schedule_text.cpp) with this Problem's names.
+
+const char* violation_name(ViolationKind k) {
+  switch (k) {
+    case ViolationKind::ComputeWithoutInputs: return "ComputeWithoutInputs";
+    case ViolationKind::CopyFromNonResident: return "CopyFromNonResident";
+    case ViolationKind::BudgetExceeded: return "BudgetExceeded";
+    case ViolationKind::FreeNonResident: return "FreeNonResident";
+    case ViolationKind::UncomputedOperator: return "UncomputedOperator";
+  }
+  return "unknown";
+}
+
+namespace {
+
+std::vector<xe_action> c_actions(const std::vector<Action>& a) {
+  std::vector<xe_action> out(a.size());
+  for (size_t k = 0; k < a.size(); ++k)
+    out[k] = {static_cast<int32_t>(a[k].kind), a[k].timestep, a[k].slot, a[k].device, a[k].op,
+              a[k].src,                        a[k].dst,      a[k].from, a[k].to};
+  return out;
+}
+
+Action cxx_action(const xe_action& x) {
+  Action a;
+  a.kind = static_cast<ActionKind>(x.kind);
+  a.timestep = x.timestep;
+  a.slot = x.slot;
+  a.device = x.device;
+  a.op = x.op;
+  a.src = x.src;
+  a.dst = x.dst;
+  a.from = x.from;
+  a.to = x.to;
+  return a;
+}
+
+struct NameTable {
+  std::vector<const char*> dev, op;
+  explicit NameTable(const Problem& p) {
+    for (const auto& d : p.devices) dev.push_back(d.id.c_str());
+    for (const auto& o : p.operators) op.push_back(o.name.c_str());
+  }
+};
+
+// a handle for the problem's structure (no copy costs needed: decode and
+// validate never price a copy)
+Handle structure_handle(const Problem& p) {
+  Problem q = p;
+  if (q.device_count() > 1 && q.copy_model.links.empty()) q.copy_model.links.push_back({-1, -1, 0.0, 1.0});
+  return upload(describe(q, std::nullopt));
+}
+
+}  // namespace
+
+Schedule decode(const Assignment& a, const Problem& p) {
+  validate_problem(p);
+  const int D = p.device_count(), T = p.op_count(), E = static_cast<int>(p.edges.size());
+  Handle h = structure_handle(p);
+  const Space sp = space_of(D, T, E);
+  std::vector<double> x(static_cast<size_t>(xe_model_cols(D, T, E)), 0.0);
+  for (const auto& [v, val] : a.values) {
+    if (v.family != VarFamily::R && v.family != VarFamily::S && v.family != VarFamily::Z && v.family != VarFamily::F)
+      continue;
+    if (v.a < 0 || v.a >= D || v.b < 0 || v.b >= T || v.c < 0 || v.c >= (v.family == VarFamily::F ? E + T : T)) continue;
+    x[static_cast<size_t>(sp.col(v))] = val;
+  }
+  int64_t n = 0;
+  xe_decode_error err{};
+  ck(xe_decode_dense(h.get(), x.data(), &n, nullptr, &err));
+  if (err.code) {
+    const auto& ops = p.operators;
+    if (err.code == 1)
+      raise(Errc::IllegalAssignment, "operator " + ops[static_cast<size_t>(err.v)].name + " at t=" + std::to_string(err.t) +
+                                         " needs tensor " + ops[static_cast<size_t>(err.u)].name + " resident on no device");
+    raise(Errc::IllegalAssignment, "copy source for tensor " + ops[static_cast<size_t>(err.u)].name +
+                                       " was freed earlier in timestep " + std::to_string(err.t));
+  }
+  std::vector<xe_action> acts(static_cast<size_t>(std::max<int64_t>(1, n)));
+  ck(xe_decode_dense(h.get(), x.data(), &n, acts.data(), &err));
+  Schedule s;
+  s.problem = p;
+  for (int64_t k = 0; k < n; ++k) s.actions.push_back(cxx_action(acts[static_cast<size_t>(k)]));
+  return s;
+}
+
+ValidationReport validate(const Schedule& s, const Problem& p, const std::vector<std::int64_t>& budgets) {
+  const int D = p.device_count();
+  std::vector<std::int64_t> bud;
+  if (budgets.empty())
+    for (const auto& d : p.devices) bud.push_back(d.budget_bytes);
+  else if (static_cast<int>(budgets.size()) == D)
+    bud = budgets;
+  else
+    raise(Errc::DimensionMismatch, "one budget per device required");
+  Handle h = structure_handle(p);
+  const auto acts = c_actions(s.actions);
+  const int64_t off[2] = {0, static_cast<int64_t>(acts.size())};
+  int64_t voff[2] = {0, 0};
+  ck(xe_validate_schedules(h.get(), acts.data(), off, 1, bud.data(), voff, nullptr));
+  std::vector<xe_violation> vs(static_cast<size_t>(std::max<int64_t>(1, voff[1])));
+  if (voff[1]) ck(xe_validate_schedules(h.get(), acts.data(), off, 1, bud.data(), voff, vs.data()));
+  ValidationReport rep;
+  const auto& ops = p.operators;
+  for (int64_t k = 0; k < voff[1]; ++k) {
+    const xe_violation& x = vs[static_cast<size_t>(k)];
+    Violation v;
+    v.kind = static_cast<ViolationKind>(x.kind);
+    v.device = x.device;
+    v.timestep = x.timestep;
+    v.slot = x.slot;
+    v.bytes = x.bytes;
+    switch (v.kind) {  // the reference's detail strings (schedule.cpp:163-231)
+      case ViolationKind::ComputeWithoutInputs:
+        v.detail = "operator " + ops[static_cast<size_t>(x.a)].name + " missing input " + ops[static_cast<size_t>(x.b)].name;
+        break;
+      case ViolationKind::CopyFromNonResident:
+      case ViolationKind::FreeNonResident:
+        v.detail = "tensor " + ops[static_cast<size_t>(x.a)].name + " not resident on " + p.devices[static_cast<size_t>(x.device)].id;
+        break;
+      case ViolationKind::BudgetExceeded:
+        v.detail = "device " + p.devices[static_cast<size_t>(x.device)].id + " holds " + std::to_string(x.bytes) +
+                   " bytes over budget " + std::to_string(bud[static_cast<size_t>(x.device)]);
+        break;
+      case ViolationKind::UncomputedOperator:
+        v.detail = "operator " + ops[static_cast<size_t>(x.a)].name + " never computed";
+        break;
+    }
+    rep.violations.push_back(v);
+  }
+  return rep;
+}
+
+double action_cost(const Problem& p, const Action& act) {
+  switch (act.kind) {
+    case ActionKind::Compute:
+      return p.operators[static_cast<size_t>(act.op)].costs_ms[static_cast<size_t>(act.device)];
+    case ActionKind::Copy: {
+      for (const auto& e : p.edges)
+        if (e.src == act.src && e.dst == act.dst) return copy_cost(p, e, act.from, act.to);
+      TensorEdge e;
+      e.src = act.src;
+      e.dst = act.dst;
+      return copy_cost(p, e, act.from, act.to);
+    }
+    case ActionKind::Free:
+    case ActionKind::Drop:
+      return 0.0;
+  }
+  return 0.0;
+}
+
+Trace replay(const Schedule& s, const Problem& p, const ModelOptions& opts, const std::optional<Assignment>& a) {
+  auto rep = validate(s, p);
+  if (!rep.ok())
+    raise(Errc::IllegalSchedule,
+          std::to_string(rep.violations.size()) + " violation(s), first: " + rep.violations.front().detail);
+  const int D = p.device_count(), T = p.op_count();
+  Handle h = upload(describe(p, opts.energy));
+  const xe_model_opts o = c_opts(opts);
+  const auto acts = c_actions(s.actions);
+  const int64_t off[2] = {0, static_cast<int64_t>(acts.size())};
+  double total = 0.0, eq1 = 0.0;
+  std::vector<int64_t> mem(static_cast<size_t>(D) * T * T), peaks(static_cast<size_t>(D));
+  ck(xe_replay_schedules(h.get(), &o, acts.data(), off, 1, &total, &eq1, mem.data(), peaks.data()));
+  Trace tr;
+  if (std::isnan(total)) {  // a copy along an undeclared edge: priced by the link model
+    total = 0.0;
+    for (const auto& act : s.actions)
+      if (act.kind == ActionKind::Compute || act.kind == ActionKind::Copy) total += action_cost(p, act);
+  }
+  tr.total_action_ms = total;
+  tr.eq1_objective_ms = a ? objective_value(*a, p, opts) : eq1;
+  tr.per_device_memory.assign(static_cast<size_t>(D), {});
+  for (int d = 0; d < D; ++d)
+    for (int t = 0; t < T; ++t)
+      for (int v = 0; v < T; ++v)
+        tr.per_device_memory[static_cast<size_t>(d)].push_back({t, v, mem[(static_cast<size_t>(d) * T + t) * T + v]});
+  tr.peaks = peaks;
+  return tr;
+}
+
+std::vector<std::pair<int, std::int64_t>> memory_timeline(const Trace& tr, int device) {
+  if (device < 0 || device >= static_cast<int>(tr.per_device_memory.size()))
+    raise(Errc::DimensionMismatch, "device index out of range");
+  std::vector<std::pair<int, std::int64_t>> out;
+  for (const auto& sample : tr.per_device_memory[static_cast<size_t>(device)]) {
+    if (out.empty() || out.back().first != sample.timestep)
+      out.push_back({sample.timestep, sample.bytes});
+    else
+      out.back().second = std::max(out.back().second, sample.bytes);
+  }
+  return out;
+}
+
+std::vector<std::pair<int, std::int64_t>> combined_memory_timeline(const Trace& tr) {
+  std::vector<std::pair<int, std::int64_t>> out;
+  for (int d = 0; d < static_cast<int>(tr.per_device_memory.size()); ++d) {
+    auto series = memory_timeline(tr, d);
+    if (out.empty()) {
+      out = series;
+    } else {
+      for (size_t i = 0; i < out.size() && i < series.size(); ++i) out[i].second += series[i].second;
+    }
+  }
+  return out;
+}
+
+std::string format_schedule(const Schedule& s) {
+  const Problem& p = s.problem;
+  Handle h = structure_handle(p);
+  const NameTable nt(p);
+  const auto acts = c_actions(s.actions);
+  size_t len = 0;
+  ck(xe_format_schedule_named(h.get(), acts.data(), static_cast<int64_t>(acts.size()), nt.dev.data(), nt.op.data(),
+                              nullptr, &len));
+  std::string out(len, '\0');
+  ck(xe_format_schedule_named(h.get(), acts.data(), static_cast<int64_t>(acts.size()), nt.dev.data(), nt.op.data(),
+                              out.data(), &len));
+  return out;
+}
+
+Schedule parse_schedule(const std::string& text, const Problem& p) {
+  Handle h = structure_handle(p);
+  const NameTable nt(p);
+  int64_t n = 0;
+  ck(xe_parse_schedule_named(h.get(), text.c_str(), nt.dev.data(), nt.op.data(), p.name.c_str(), nullptr, &n));
+  std::vector<xe_action> acts(static_cast<size_t>(std::max<int64_t>(1, n)));
+  ck(xe_parse_schedule_named(h.get(), text.c_str(), nt.dev.data(), nt.op.data(), p.name.c_str(), acts.data(), &n));
+  Schedule s;
+  s.problem = p;
+  for (int64_t k = 0; k < n; ++k) s.actions.push_back(cxx_action(acts[static_cast<size_t>(k)]));
+  return s;
+}
+
+std::string trace_csv(const Trace& tr, const Problem& p) {
+  std::string out = "device,timestep,slot,bytes\n";
+  for (int d = 0; d < static_cast<int>(tr.per_device_memory.size()); ++d)
+    for (const auto& sample : tr.per_device_memory[static_cast<size_t>(d)])
+      out += p.devices[static_cast<size_t>(d)].id + "," + std::to_string(sample.timestep) + "," +
+             std::to_string(sample.slot) + "," + std::to_string(sample.bytes) + "\n";
+  return out;
 }
 
 }  // namespace xengine

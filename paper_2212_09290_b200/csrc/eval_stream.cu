@@ -195,6 +195,7 @@ void il_to_canon_device(const xe_problem* pr, const uint64_t* il, int64_t first,
 bool stream_supported(const xe_problem* pr, const xe_model_opts& opts) {
   const HostProblem& h = pr->h;
   if (opts.use_energy && h.has_energy) return false;  // energy terms/rows: the exact kernels
+  if (pr->exact_objective) return false;               // reference order requested
   if (!il_layout_ok(pr) || h.E >= 65536) return false;
   return static_cast<size_t>(h.E) * h.D * h.D * 8 <= 64 * 1024;  // copy table in shared memory
 }

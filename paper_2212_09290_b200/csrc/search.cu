@@ -146,7 +146,7 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
   std::memset(res, 0, sizeof *res);
   res->objective = res->rounding_objective = INFINITY;
   res->index = -1;
-  res->lp_bound = NAN;
+  res->lp_bound = res->lp_value = NAN;
   res->lp_certified = 1;
 
   // ---- K1 + K3: LP relaxation, its x on the device for the rounding
@@ -168,8 +168,15 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     check_rc(xe_pdhg_solve(m, &po, &lr, xh.data(), nullptr));
     x.upload(xh, s);
     res->has_lp = 1;
-    res->lp_bound = lr.primal_obj;
+    // the Lagrangian dual value b'y + sum_j min over [lb_j, ub_j] of the
+    // reduced-cost term (every column is boxed, y is sign-projected) is a
+    // lower bound of the presolved LP for ANY iterate, converged or not; it
+    // bounds the full LP (and so the MILP) only when the prohibitive-cost
+    // fixing is certified by the same duals
+    res->lp_value = lr.primal_obj;
+    res->lp_converged = lr.status == 0;
     res->lp_certified = lr.certified;
+    res->lp_bound = lr.certified ? std::min(lr.dual_obj, lr.primal_obj) : -INFINITY;
   }
 
   // ---- rounding rounds
@@ -336,7 +343,11 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
   xe_eval_out eo{o1.p, p1.p, f1.p};
   xe_best b{};
   check_rc(xe_eval_cubes(pr, &mo, inc.p, 1, &eo, mask, &b, s));
-  if (b.index != 0 || b.obj != res->objective) fail(XE_ERR_ARG, "search: incumbent re-evaluation mismatch");
+  // the batch scores may be the streaming evaluator's reassociated sums (within
+  // #terms * 2^-53 relative); the single re-score is the reference's order
+  if (b.index != 0 || !(std::fabs(b.obj - res->objective) <= 1e-9 * std::max(1.0, std::fabs(b.obj))))
+    fail(XE_ERR_ARG, "search: incumbent re-evaluation mismatch");
+  res->objective = b.obj;
   if (cube_host) XE_CUDA(cudaMemcpyAsync(cube_host, inc.p, words * 4, cudaMemcpyDeviceToHost, s));
   if (peaks_host) XE_CUDA(cudaMemcpyAsync(peaks_host, p1.p, h.D * 8, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaStreamSynchronize(s));

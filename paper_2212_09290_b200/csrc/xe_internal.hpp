@@ -190,6 +190,11 @@ struct xe_problem {
   };
   Stage stage[2];
   xe::DevBuf<uint64_t> chunk_best;  // [chunks][3] best-of-chunk triples
+  // objective order of the batched evaluators: false = the streaming
+  // evaluator's per-timestep reassociation (within #terms * 2^-53 relative,
+  // best-of-batch re-scored exactly), true = the reference's order for every
+  // candidate (the reference-order kernels)
+  bool exact_objective = false;
 };
 
 namespace xe {

@@ -52,7 +52,7 @@ class SearchResult:
                                 # search can still find a schedule from over-budget candidates)
     cube: Optional[np.ndarray]  # the final incumbent's canonical (R, S) cube, uint32 words
     peaks: Optional[np.ndarray]  # per-device peak bytes of the incumbent
-    lp_bound: Optional[float]   # PDHG LP relaxation value (lower bound), None without LP
+    lp_bound: Optional[float]   # certified lower bound from the PDHG duals (Lagrangian value), None without LP
     lp_certified: bool
     n_evaluated: int
     n_valid: int                # valid rounding candidates

@@ -24,6 +24,7 @@
 #include "xengine/mps_io.hpp"
 #include "xengine/model.hpp"
 #include "xengine/problem.hpp"
+#include "xengine/schedule.hpp"
 #include "xengine/solver.hpp"
 #include "xengine_b200.h"
 
@@ -88,6 +89,29 @@ void run(const char* name, const std::function<void()>& body) {
 std::map<ConstraintTag, int> census(const MilpModel& m) {
   std::map<ConstraintTag, int> n;
   for (const auto& c : m.constraints) ++n[c.tag];
+  return n;
+}
+
+// proj/tests/test_solver.cpp:29-44
+Problem long_chain(int n, int devices) {
+  Problem p;
+  p.name = "chain" + std::to_string(n);
+  for (int d = 0; d < devices; ++d) p.devices.push_back({"dev" + std::to_string(d), std::int64_t(n) * kMiB, {}});
+  for (int i = 0; i < n; ++i) {
+    OperatorNode op;
+    op.name = "op" + std::to_string(i);
+    op.output_bytes = kMiB;
+    op.costs_ms.assign(size_t(devices), 1.0);
+    p.operators.push_back(op);
+    if (i > 0) p.edges.push_back({i - 1, i, {}});
+  }
+  p.copy_model.links.push_back({-1, -1, 0.125, double(1 << 30)});
+  return p;
+}
+int count_r(const Assignment& a) {
+  int n = 0;
+  for (const auto& [v, x] : a.values)
+    if (v.family == VarFamily::R && x > 0.5) ++n;
   return n;
 }
 
@@ -388,6 +412,125 @@ void device_cases() {
     CHECK(s.assignment.at(var_r(0, 1, 1)) == 1.0);
     CHECK(s.assignment.objective_reported == 11.0);
     CHECK(check_assignment(build_model(p), s.assignment).empty());
+  });
+  // ---- solve_exact: proj/tests/test_solver.cpp:66-190
+  run("solve_exact: chain3 = 9.0 with the identity R", [] {
+    Problem p = fixture("chain3");
+    Solution s = solve_exact(p);
+    CHECK(s.status == SolveStatus::Optimal);
+    CHECK(s.backend == "exact");
+    CHECK(s.objective_ms == 9.0);
+    CHECK(s.assignment.objective_reported == 9.0);
+    for (int t = 0; t < 3; ++t)
+      for (int i = 0; i < 3; ++i) CHECK(s.assignment.at(var_r(0, t, i)) == (t == i ? 1.0 : 0.0));
+    CHECK(count_r(s.assignment) == 3);
+  });
+  run("solve_exact: chain3 infeasible at 3 MiB, 9.0 at 8 MiB", [] {
+    Problem p = fixture("chain3");
+    CHECK(solve_exact(p, {}, {3 * kMiB}).status == SolveStatus::Infeasible);
+    Solution ok = solve_exact(p, {}, {8 * kMiB});
+    CHECK(ok.status == SolveStatus::Optimal);
+    CHECK(ok.objective_ms == 9.0);
+  });
+  run("solve_exact: fig2 = 11 with the reference's twin (A on the gpu)", [] {
+    Problem p = fixture("fig2");
+    Solution s = solve_exact(p);
+    CHECK(s.status == SolveStatus::Optimal);
+    CHECK(s.objective_ms == 11.0);
+    CHECK(s.assignment.at(var_r(0, 0, 0)) == 1.0);
+    CHECK(s.assignment.at(var_r(1, 1, 1)) == 1.0);
+    CHECK(s.assignment.at(var_r(0, 6, 6)) == 1.0);
+    CHECK(check_assignment(build_model(p), s.assignment).empty());
+    CHECK(s.nodes_explored > 1000);
+  });
+  run("solve_exact: chain_lowmem sweep 24/24/24/24/27, 12 computes at 25 %", [] {
+    Problem p = fixture("chain_lowmem");
+    CHECK(save_all_budget(p) == 34 * kMiB);
+    const double pct[5] = {100, 65, 50, 35, 25}, want[5] = {24, 24, 24, 24, 27};
+    for (int k = 0; k < 5; ++k) {
+      Solution s = solve_exact(p, {}, {budget_percent(save_all_budget(p), pct[k])});
+      CHECK(s.status == SolveStatus::Optimal);
+      CHECK(s.objective_ms == want[k]);
+    }
+    Solution tight = solve_exact(p, {}, {budget_percent(save_all_budget(p), 25.0)});
+    CHECK(count_r(tight.assignment) == 12);
+    CHECK(solve_exact(p, {}, {10 * kMiB}).objective_ms == 24.0);
+    CHECK(solve_exact(p, {}, {9 * kMiB}).objective_ms == 27.0);
+    CHECK(solve_exact(p, {}, {8 * kMiB}).objective_ms == 27.0);
+    CHECK(solve_exact(p, {}, {4 * kMiB - 1}).status == SolveStatus::Infeasible);
+  });
+  run("solve_exact: limits return LimitReached", [] {
+    Problem p = fixture("fig2");
+    SearchLimits one;
+    one.node_limit = 1;
+    CHECK(solve_exact(p, {}, {}, one).status == SolveStatus::LimitReached);
+    SearchLimits some;
+    some.node_limit = 3000;
+    Solution part = solve_exact(p, {}, {}, some);
+    CHECK(part.status == SolveStatus::LimitReached);
+    CHECK(part.nodes_explored <= 3000 + 1);
+    SearchLimits instant;
+    instant.time_limit_ms = 0;
+    CHECK(solve_exact(p, {}, {}, instant).status == SolveStatus::LimitReached);
+  });
+  run("solve_exact: TooLarge beyond 64 residency bits; a 12-op chain on one device", [] {
+    CHECK_THROWS_CODE(solve_exact(long_chain(33, 2)), Errc::TooLarge);
+    CHECK(solve_exact(long_chain(12, 1)).status == SolveStatus::Optimal);
+    CHECK_THROWS_CODE(assignment_oracle(long_chain(23, 2)), Errc::TooLarge);
+    CHECK(assignment_oracle(long_chain(23, 1)).status == SolveStatus::Optimal);
+  });
+  // ---- schedule.hpp: proj/tests/test_schedule.cpp:300-370
+  run("replay accounts costs and memory (fig2 exact optimum)", [] {
+    Problem p = fixture("fig2");
+    Solution sol = solve_exact(p);
+    Schedule s = decode(sol.assignment, p);
+    CHECK(validate(s, p).ok());
+    Trace with_a = replay(s, p, {}, sol.assignment);
+    CHECK(with_a.total_action_ms == 11.0);
+    CHECK(with_a.eq1_objective_ms == 11.0);
+    Trace bare = replay(s, p);
+    CHECK(bare.eq1_objective_ms == with_a.eq1_objective_ms);
+    CHECK(bare.total_action_ms == with_a.total_action_ms);
+    CHECK(with_a.per_device_memory.size() == 2);
+    CHECK(with_a.per_device_memory[0].size() == 49);
+    CHECK(with_a.peaks[0] == 8 * kMiB);
+    CHECK(with_a.peaks[1] == 32 * kMiB);
+    auto c = combined_memory_timeline(with_a);
+    auto a0 = memory_timeline(with_a, 0), a1 = memory_timeline(with_a, 1);
+    bool sum = c.size() == a0.size();
+    for (size_t t = 0; sum && t < c.size(); ++t) sum = c[t].second == a0[t].second + a1[t].second;
+    CHECK(sum);
+    // text round trip
+    Schedule back = parse_schedule(format_schedule(s), p);
+    CHECK(back.actions == s.actions);
+    CHECK(trace_csv(with_a, p).rfind("device,timestep,slot,bytes\ncpu,0,0,", 0) == 0);
+  });
+  run("memory timelines match the hand-computed chains", [] {
+    Problem p = fixture("chain3");
+    Solution sol = solve_exact(p);
+    Trace lean = replay(decode(sol.assignment, p), p, {}, sol.assignment);
+    using Series = std::vector<std::pair<int, std::int64_t>>;
+    CHECK(memory_timeline(lean, 0) == (Series{{0, 4 * kMiB}, {1, 8 * kMiB}, {2, 8 * kMiB}}));
+    Assignment all = save_all_assignment(p, {0, 0, 0});
+    Trace fat = replay(decode(all, p), p, {}, all);
+    CHECK(memory_timeline(fat, 0) == (Series{{0, 4 * kMiB}, {1, 8 * kMiB}, {2, 12 * kMiB}}));
+    CHECK(combined_memory_timeline(fat) == memory_timeline(fat, 0));
+    CHECK_THROWS(memory_timeline(fat, 1));
+  });
+  run("replay refuses illegal schedules; validate reports them", [] {
+    Problem p = fixture("chain3");
+    Schedule s = decode(solve_exact(p).assignment, p);
+    s.actions.erase(s.actions.begin());
+    CHECK_THROWS_CODE(replay(s, p), Errc::IllegalSchedule);
+    ValidationReport rep = validate(s, p);
+    CHECK(!rep.ok());
+    CHECK_THROWS_CODE(validate(s, p, {kMiB, kMiB}), Errc::DimensionMismatch);
+  });
+  run("action costs", [] {
+    Problem p = fixture("fig2");
+    CHECK(action_cost(p, Action{ActionKind::Compute, 1, 0, 1, 1, -1, -1, -1, -1}) == 3.0);
+    CHECK(action_cost(p, Action{ActionKind::Copy, 1, 0, -1, -1, 0, 1, 0, 1}) == 1.0);
+    CHECK(action_cost(p, Action{ActionKind::Free, 1, 1, 1, -1, 0, 1, -1, -1}) == 0.0);
   });
   run("solve_search: F1 chain3 = 9.0, proven by the LP bound", [] {
     Problem p = fixture("chain3");

@@ -58,7 +58,7 @@ def test_local_search_neighbours(oracle):
     the GPU evaluation of every neighbour."""
     text = configs.vgg16_doc()
     a = xo.arrays_from_json(text)
-    prob = xe.Problem.from_json(text)
+    prob = xe.Problem.from_json(text).set_exact_objective()  # objective bits compared with the oracle
     base = xe.round_cubes(prob, 1, seed=4)[0]
     nb = xe.mutate_cubes(prob, base, 512, seed=9, edits=2)
     again = torch.cat([xe.mutate_cubes(prob, base, 200, seed=9, edits=2),
@@ -109,7 +109,7 @@ def test_move_cubes_canonical_saves(oracle, name):
     from cubegen import unpack
     text = golden_problem_text(name) if name == "fig2" else configs.CONFIGS[name]()
     a = xo.arrays_from_json(text)
-    prob = xe.Problem.from_json(text)
+    prob = xe.Problem.from_json(text).set_exact_objective()  # objective bits compared with the oracle
     n = 32 if name == "resnet50" else 200
     base = xe.round_cubes(prob, n, seed=3, edits=4, perturb=0.0)
     canon = xe.move_cubes(prob, base, n, 0, max_moves=0)
@@ -133,7 +133,7 @@ def test_move_cubes_canonical_saves(oracle, name):
 def test_move_cubes_neighbours(oracle):
     from cubegen import unpack
     a = xo.arrays_from_json(configs.vgg16_doc())
-    prob = xe.Problem.from_json(configs.vgg16_doc())
+    prob = xe.Problem.from_json(configs.vgg16_doc()).set_exact_objective()  # objective bits compared with the oracle
     bases = xe.move_cubes(prob, xe.round_cubes(prob, 4, seed=9, edits=3, perturb=0.0), 4, 0, max_moves=0)
     nb = xe.move_cubes(prob, bases, 4 * 256, 21, first=0, max_moves=3)
     # pure function of (seed, index, base); chains map to blocks of 256

@@ -72,11 +72,22 @@ def test_vgg16_bench_scale_batch_rescored_by_reference(ref):
     cubes = xe.round_cubes(prob, n, seed=2212, edits=3, perturb=0.1)
     il = xe.cubes_to_il(prob, cubes)
     res = xe.evaluate_cubes_il(prob, il, n, valid_mask=_MASK)
-    pick = np.unique(np.concatenate([np.random.default_rng(5).choice(n, 64, replace=False), [res.best_index]]))
+    # the GPU top-64 valid candidates, a deterministic sample, the winner
+    ok = (res.flags.to(torch.int64) & _MASK) == 0
+    top = torch.argsort(torch.where(ok, res.obj, torch.full_like(res.obj, float("inf"))), stable=True)[:64]
+    pick = np.unique(np.concatenate([np.random.default_rng(5).choice(n, 64, replace=False), top.cpu().numpy(),
+                                     [res.best_index]]))
     host = cubes[torch.from_numpy(pick).cuda()].cpu().numpy().view(np.uint32)
     ro, rpk, rf = rp.eval_cubes(host, prob.D, nthreads=8)
     sel = torch.from_numpy(pick).cuda()
-    assert np.array_equal(ro.view(np.int64), res.obj[sel].cpu().numpy().view(np.int64))
+    go = res.obj[sel].cpu().numpy()
+    if prob.objective_order_exact:
+        assert np.array_equal(ro.view(np.int64), go.view(np.int64))
+    else:  # the streaming evaluator's reassociation: within #terms * 2^-53 (stated bound 1e-12)
+        assert np.all(np.abs(go - ro) <= 1e-12 * np.abs(ro)), np.max(np.abs(go - ro) / np.abs(ro))
+    # the reference's first minimum over the re-scored set is the GPU winner, same bits
+    rv = np.where(ref_flags_valid(rf), ro, np.inf)
+    assert pick[int(np.argmin(rv))] == res.best_index and rv.min() == res.best_obj
     assert np.array_equal(rpk, res.peak[sel].cpu().numpy())
     f = res.flags[sel].cpu().numpy().astype(np.uint32)
     rf = rf.astype(np.uint32)
