@@ -68,16 +68,34 @@ def issue_roofline(config, cand_per_s, clocks):
             "ncu_issue_active_pct": d.get("issue_active_pct")}
 
 
+def k4_sample(doc, m):
+    """The first m candidates of the GPU arm's own workload (K4 round_cubes,
+    seed 2212, 3 edits, 10 % flips: the same Philox indices), canonical
+    layout on the host; the numpy mix of tests/cubegen.py without a GPU."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            import paper_2212_09290_b200 as xe
+            prob = xe.Problem.from_json(doc)
+            return xe.round_cubes(prob, m, SEED, edits=3, perturb=0.1).cpu().numpy().view(np.uint32), "k4"
+    except Exception:
+        pass
+    from oracle import xo
+    import cubegen
+    return cubegen.mixed_cubes(xo.arrays_from_json(doc), m, seed=SEED, random_frac=0.0), "cubegen"
+
+
 def cpu_reference_rate(doc, a, seconds=12.0, nthreads=None, cubes=None):
     """Reference library (oracle/_ref) on the host cores: per candidate
-    complete_assignment + objective_value + check_assignment + peaks."""
+    complete_assignment + objective_value + check_assignment + peaks + decode
+    legality (what K2 computes per candidate)."""
     from oracle import xo
     import cubegen
     nthreads = nthreads or os.cpu_count() or 1
     if xo.ref_available():
         rp = xo.Ref().load(doc)
         kind = "reference"
-        run = lambda c: rp.eval_cubes(c, a.D, check=True, decode=False, nthreads=nthreads)
+        run = lambda c: rp.eval_cubes(c, a.D, check=True, decode=True, nthreads=nthreads)
     else:  # the C restatement, one thread
         orc = xo.Oracle()
         kind, nthreads = "port", 1
@@ -94,6 +112,139 @@ def cpu_reference_rate(doc, a, seconds=12.0, nthreads=None, cubes=None):
     return done / el, kind, nthreads, done, el
 
 
+def _timed(fn, warmup=1, reps=3):
+    """median wall time of fn() in seconds after warmup calls (CUDA-synchronised)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)), r
+
+
+def _event_ms(fn, reps=3, warmup=1, stream=None):
+    """mean CUDA-event time of fn() on the current stream, ms."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        r = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, r
+
+
+def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
+    """One dense-cube config (3 ResNet-50 / 4 U-Net) on one GPU: K1 model, K3
+    PDHG to 1e-7 (HBM roofline of the half-steps), K4 LP-guided rounding and
+    the K2 evaluation of the rounded batch (HBM roofline of the evaluator)."""
+    import torch
+    import paper_2212_09290_b200 as xe
+    prob = xe.Problem.from_json(doc_fn())
+    k1_wall, model = _timed(lambda: xe.build_model(prob), warmup=1, reps=1)
+    lp = xe.pdhg_solve(model, tol=1e-7, max_iters=1000000, return_x=True)
+    it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
+    x = torch.from_numpy(lp.x).cuda()
+    gen_ms, cubes = _event_ms(lambda: xe.round_cubes(prob, n, SEED, edits=3, perturb=0.0, x=x), reps=1)
+    il = xe.cubes_to_il(prob, cubes)
+    del cubes
+    mask = _lib_mask()
+    out = (torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty((n, prob.D), dtype=torch.int64, device="cuda"),
+           torch.empty(n, dtype=torch.int32, device="cuda"))
+    ev_ms, r = _event_ms(lambda: xe.evaluate_cubes_il(prob, il, n, valid_mask=mask, out=out, best=False), reps=5)
+    bpc = 2 * prob.D * prob.T * ((prob.T + 63) // 64) * 8 + 8 + 8 * prob.D + 4
+    ev_gbs = n * bpc / (ev_ms / 1e3) / 1e9
+    d = {"workload": f"{name}: T={prob.T}, E={prob.E}, D={prob.D}",
+         "k1_build": {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "device_ms": model.build_ms(),
+                      "wall_ms": 1e3 * k1_wall,
+                      "achieved_gbs": (12 * model.nnz + 8 * (model.n_rows + 1) + 26 * model.n_cols) / (model.build_ms() / 1e3) / 1e9},
+         "pdhg": {"metric": "PDHG iters/sec", "iters": lp.iters, "converged": lp.converged, "certified": lp.certified,
+                  "iters_per_s": lp.iters / (lp.solve_ms / 1e3), "time_to_tol_ms": lp.solve_ms, "tol": 1e-7,
+                  "objective": lp.primal_obj, "dual_bound": lp.dual_obj,
+                  "roofline": {"bound": "hbm", "bytes_per_iter": it_bytes,
+                               "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                               "frac": it_bytes / (lp.ms_per_iter / 1e3) / 1e9 / hbm}},
+         "k4_rounding": {"candidates": n, "candidates_per_s": n / (gen_ms / 1e3)},
+         "k2_eval": {"candidates": n, "candidates_per_s": n / (ev_ms / 1e3), "kernel_ms": ev_ms,
+                     "layout": "xe_cube_il", "bytes_per_candidate": bpc,
+                     "roofline": {"bound": "hbm", "achieved": ev_gbs, "peak": hbm, "unit": "GB/s", "frac": ev_gbs / hbm}}}
+    if want_lp is not None:
+        d["pdhg"]["highs_objective"] = want_lp
+        d["pdhg"]["rel_err"] = abs(lp.primal_obj - want_lp) / want_lp
+    if highs_recorded is not None:
+        d["pdhg"]["highs_seconds_recorded"] = highs_recorded
+    return d, prob
+
+
+def placement_config(n, hbm):
+    """Config 5 (random 2000-op DAG, D=8): K2b save-all placement sweep over n
+    resident placements; HBM roofline plus the shared-memory gather roofline
+    (every op and edge term is one gather of the per-device tables)."""
+    import torch
+    import paper_2212_09290_b200 as xe
+    from bench import configs
+    prob = xe.Problem.from_json(configs.random2000_doc())
+    dev = xe.random_placements(prob, n, SEED)
+    out = (torch.empty(n, dtype=torch.float64, device="cuda"), torch.empty((n, prob.D), dtype=torch.int64, device="cuda"),
+           torch.empty(n, dtype=torch.int32, device="cuda"))
+    ms, r = _event_ms(lambda: xe.evaluate_placements(prob, dev, policy=0, out=out), reps=5)
+    bpc = prob.T + 8 + 8 * prob.D + 4
+    rate = n / (ms / 1e3)
+    gbs = rate * bpc / 1e9
+    # gathers per placement: T compute-cost + T mass + E (src, dst device pair -> copy table)
+    gathers = 2 * prob.T + prob.E
+    props = torch.cuda.get_device_properties(0)
+    sm_clock_ghz = 1.965
+    lds_peak = props.multi_processor_count * 32 * sm_clock_ghz * 1e9  # one 4-byte shared-memory lane access per bank per clock
+    return {"workload": f"random2000 cfg5: T={prob.T}, E={prob.E}, D={prob.D}, save-all placements",
+            "placements": n, "placements_per_s": rate, "kernel_ms": ms, "sweep_1e9_seconds": 1e9 / rate,
+            "best": {"obj_ms": r.best_obj, "index": r.best_index},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                         "bytes_per_candidate": bpc},
+            "gather_roofline": {"bound": "smem gather", "gathers_per_placement": gathers,
+                                "achieved": rate * gathers, "peak": lds_peak, "unit": "gathers/s",
+                                "frac": rate * gathers / lds_peak,
+                                "peak_note": "148 SMs x 32 banks x 1 access/clock at 1965 MHz"}}
+
+
+def reference_inrun(doc_vgg, doc_resnet):
+    """The reference's own K1 (build_model) and MPS writer (write_mps) timed
+    in this run on the host (oracle/_ref, one thread), and HiGHS on the
+    VGG-16 LP relaxation (SciPy linprog on the reference model)."""
+    from oracle import xo
+    out = {}
+    if not xo.ref_available():
+        return {"unavailable": "oracle/_ref not built"}
+    R = xo.Ref()
+    for name, doc in (("vgg16", doc_vgg), ("resnet50", doc_resnet)):
+        rp = R.load(doc)
+        t0 = time.perf_counter()
+        rp.model_csr()
+        t_build = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        mps = rp.write_mps()
+        t_mps = time.perf_counter() - t0
+        out[name] = {"build_model_ms": 1e3 * t_build, "build_model_plus_write_mps_ms": 1e3 * t_mps,
+                     "mps_bytes": len(mps), "threads": 1}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from gen_lp_golden import lp_value
+        v, dt = lp_value(xo.arrays_from_json(doc_vgg))
+        out["vgg16"]["highs_lp_seconds"] = dt
+        out["vgg16"]["highs_lp_objective"] = v
+    except Exception as ex:  # scipy/HiGHS missing on the host
+        out["vgg16"]["highs_lp_unavailable"] = str(ex)[:200]
+    return out
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -104,7 +255,7 @@ def reference_arm(args):
     doc = configs.vgg16_doc()
     a = xo.arrays_from_json(doc)
     nthreads = os.cpu_count() or 1
-    cubes = cubegen.mixed_cubes(a, max(64, 16 * nthreads), seed=SEED, random_frac=0.0)
+    cubes, source = k4_sample(doc, max(64, 16 * nthreads))
     step_s = float(os.environ.get("XE_REF_STEP_S", "4"))
     for _ in range(args.warmup):
         cpu_reference_rate(doc, a, seconds=0.5, nthreads=nthreads, cubes=cubes)
@@ -118,11 +269,12 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
-        "data": "synthetic (bench/configs.py vgg16_doc; tests/cubegen.py mixed candidates, seed 2212)",
+        "data": f"synthetic: the GPU arm's first candidates ({source}: K4 round_cubes, Philox seed 2212, "
+                "3 edits, 10% flips)",
         "config": {"workload": WORKLOAD, "sample_per_step": int(np.mean(counts))},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
                          "sample": f"{int(np.mean(counts))} VGG-16 candidates per step, "
-                                   "complete_assignment+objective_value+check_assignment+peaks"},
+                                   "complete_assignment+objective_value+check_assignment+peaks+decode"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -178,7 +330,7 @@ def resnet_pipeline(args):
             "k1_build": {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "ms": model.build_ms()},
             "pdhg": {"iters": lp.iters, "converged": lp.converged, "certified": lp.certified,
                      "iters_per_s": lp.iters / (lp.solve_ms / 1e3), "time_to_tol_ms": lp.solve_ms, "tol": 1e-7,
-                     "objective": lp.primal_obj, "highs_objective": want, "highs_seconds": 651.6,
+                     "objective": lp.primal_obj, "highs_objective": want, "highs_seconds_recorded": 565.3,
                      "rel_err": abs(lp.primal_obj - want) / want,
                      "roofline": {"bound": "hbm", "bytes_per_iter": it_bytes,
                                   "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}},
@@ -293,6 +445,7 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-pdhg", action="store_true")
     ap.add_argument("--skip-search", action="store_true")
+    ap.add_argument("--skip-configs", action="store_true", help="skip the config 3/4/5 objects of the default line")
     ap.add_argument("--workload", default="vgg16", choices=["vgg16", "random2000", "resnet50"],
                     help="vgg16: BASELINE config 2 (the headline); random2000: config 5 placement sweep; "
                          "resnet50: config 3 (K1 + PDHG LP + LP-guided rounding + evaluation)")
@@ -487,16 +640,41 @@ def main():
             "objective": sr.objective, "reference_milp_optimum": opt, "equal_to_reference": sr.objective == opt,
             "peaks": [int(v) for v in sr.peaks] if sr.peaks is not None else None,
             "reference_peaks": [26894336, 60411904], "lp_bound": sr.lp_bound, "rounding_objective": sr.rounding_objective,
-            "candidates_evaluated": sr.n_evaluated, "seconds": dt, "reference_seconds": 86.0}
+            "candidates_evaluated": sr.n_evaluated, "seconds": dt,
+            "reference_milp_seconds_recorded": {"seconds": 86.0, "how": "solve_external + HiGHS MILP on the reference "
+                                                                    "MPS, survey-measured (SURVEY §8c cfg-2 row); too "
+                                                                    "slow to repeat inside the bench"}}
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----
+    # ---- the other BASELINE configs on this GPU (rank 0, N = 1): 3 ResNet-50,
+    # 4 U-Net (K1 + K3 + K4 + K2 on the dense cube path), 5 random 2000-op
+    # (K2b placements), and the reference's own K1 / MPS / HiGHS in this run
+    if rank == 0 and world == 1 and not args.skip_configs:
+        hbm_gbs = peaks()[0]
+        r = None
+        del il, out, obj, pk, fl
+        torch.cuda.empty_cache()
+        line["cfg3_resnet50"], _ = dense_config("resnet50-train cfg3 (Appendix B seed 3)", configs.resnet50_doc,
+                                                1 << 20, hbm_gbs, want_lp=107.49787109375002,
+                                                highs_recorded={"seconds": 565.3, "method": "highs-ipm",
+                                                                "source": "tests/golden/lp_values.json (this container)"})
+        line["cfg4_unet"], _ = dense_config("unet-train cfg4 (Appendix B seed 4)", configs.unet_doc, 1 << 20,
+                                            hbm_gbs)
+        line["cfg5_random2000"] = placement_config(4_000_000, hbm_gbs)
+        line["reference_inrun"] = reference_inrun(doc, configs.resnet50_doc())
+
+    # ---- CPU baseline (rank 0, N = 1 only): the reference on this host's cores
+    # over the first candidates of this very workload
     if rank == 0 and world == 1 and not args.skip_cpu:
         from oracle import xo
         a = xo.arrays_from_json(doc)
-        rate, kind, nt, done, el = cpu_reference_rate(doc, a, seconds=12.0)
+        nt_all = os.cpu_count() or 1
+        sample, source = k4_sample(doc, max(64, 16 * nt_all))
+        rate, kind, nt, done, el = cpu_reference_rate(doc, a, seconds=12.0, cubes=sample)
+        rate1, _, _, done1, el1 = cpu_reference_rate(doc, a, seconds=3.0, nthreads=1, cubes=sample[:64])
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": nt, "kind": kind,
-                                "sample": f"{done} VGG-16 candidates in {el:.1f}s (complete_assignment+"
-                                          "objective_value+check_assignment+peaks per candidate)"}
+                                "sample": f"{done} VGG-16 candidates of this workload ({source}) in {el:.1f}s "
+                                          "(complete_assignment+objective_value+check_assignment+peaks+decode)",
+                                "one_core": {"value": rate1, "unit": UNIT, "sample": f"{done1} in {el1:.1f}s"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
