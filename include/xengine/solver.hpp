@@ -19,6 +19,8 @@
 
 #include "xengine/model.hpp"
 
+struct xe_ctx;  // include/xengine_b200.h
+
 namespace xengine {
 
 enum class SolveStatus { Optimal, Infeasible, LimitReached };
@@ -76,5 +78,11 @@ struct SearchParams {
 // was found: infeasibility is not proven); nodes_explored = candidates
 // scored.  The assignment is complete_assignment of the best (R, S).
 Solution solve_search(const Problem& p, const ModelOptions& opts = {}, const SearchParams& params = {});
+
+// The same search sharded over the ranks of a native multi-GPU context
+// (xe_ctx of include/xengine_b200.h: one per GPU, NCCL underneath): rounding
+// blocks interleaved by rank, one local-search population per rank, the
+// global first-minimum incumbent; every rank returns the same Solution.
+Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchParams& params, xe_ctx* ctx);
 
 }  // namespace xengine

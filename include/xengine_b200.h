@@ -508,6 +508,31 @@ int xe_parse_schedule_named(const xe_problem* p, const char* text, const char* c
                             const char* const* op_names, const char* problem_name, xe_action* actions,
                             int64_t* n_actions);
 
+/* ---- multi-GPU from the C / C++ host -------------------------------------
+ * One xe_ctx per GPU (device, rank, world, NCCL communicator, stream), used
+ * by one host thread at a time.  Rank 0 creates the id (xe_nccl_unique_id)
+ * and the caller distributes it (MPI, a file, torch.distributed ...).  The
+ * candidate sweeps shard with no data-path collective; the exchanges are the
+ * incumbent's (all-reduce MIN of the objective bits, MIN of the global index
+ * among ranks holding it, SUM of valid counts: the first-minimum rule of
+ * solver.cpp:57-61 across ranks) and the winning schedule's broadcast.
+ * NCCL is loaded at xe_ctx_create (libnccl.so.2); errors: XE_ERR_NCCL. */
+#define XE_NCCL_ID_BYTES 128
+typedef struct xe_ctx xe_ctx;
+int xe_nccl_unique_id(uint8_t* id /* [XE_NCCL_ID_BYTES] */);
+int xe_ctx_create(int device, int rank, int world, const uint8_t* id, xe_ctx** out);
+int xe_ctx_destroy(xe_ctx* c);
+int xe_ctx_info(const xe_ctx* c, int32_t* device, int32_t* rank, int32_t* world);
+/* best: this rank's best-of-batch (index local to its shard) -> the global
+ * one; index_offset = the shard's first global index. */
+int xe_ctx_exchange_best(xe_ctx* c, int64_t index_offset, xe_best* best);
+/* xe_search sharded over the context's ranks (rank/world of so are set from
+ * the context): rounding blocks interleaved by rank, one local-search
+ * population per rank, the global rounding incumbent, the best final
+ * schedule (the rounding incumbent on ties) broadcast to every rank. */
+int xe_search_dist(const xe_problem* p, const xe_model_opts* opts, const xe_search_opts* so, xe_ctx* c,
+                   xe_search_result* res, uint32_t* cube_host, int64_t* peaks_host);
+
 #ifdef __cplusplus
 }
 #endif

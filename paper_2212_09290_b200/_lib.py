@@ -207,6 +207,12 @@ SIGNATURES = {
                                  P, P]),
     "xe_exact_opts_default": (None, [C.POINTER(ExactOpts)]),
     "xe_decode_cubes": (C.c_int, [P, C.POINTER(ModelOpts), P, C.c_int64, P, P, P]),
+    "xe_nccl_unique_id": (C.c_int, [P]),
+    "xe_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "xe_ctx_destroy": (C.c_int, [P]),
+    "xe_ctx_info": (C.c_int, [P, P, P, P]),
+    "xe_ctx_exchange_best": (C.c_int, [P, C.c_int64, C.POINTER(Best)]),
+    "xe_search_dist": (C.c_int, [P, C.POINTER(ModelOpts), C.POINTER(SearchOpts), P, C.POINTER(SearchResult), P, P]),
     "xe_decode_dense": (C.c_int, [P, P, C.POINTER(C.c_int64), P, P]),
     "xe_validate_schedules": (C.c_int, [P, P, P, C.c_int64, P, P, P]),
     "xe_replay_schedules": (C.c_int, [P, C.POINTER(ModelOpts), P, P, C.c_int64, P, P, P, P]),

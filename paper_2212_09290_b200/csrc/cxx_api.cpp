@@ -997,6 +997,10 @@ Solution solve_exact(const Problem& p, const ModelOptions& opts, std::vector<std
 }
 
 Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchParams& params) {
+  return solve_search(p, opts, params, nullptr);
+}
+
+Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchParams& params, xe_ctx* ctx) {
   validate_problem(p);
   const int D = p.device_count(), T = p.op_count();
   Handle h = upload(describe(p, opts.energy));
@@ -1017,7 +1021,10 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
   xe_search_result r{};
   std::vector<uint32_t> cube(xe_cube_bytes(D, T) / 4);
   std::vector<int64_t> peaks(static_cast<size_t>(D));
-  ck(xe_search(h.get(), &o, &so, &r, cube.data(), peaks.data(), nullptr));
+  if (ctx)
+    ck(xe_search_dist(h.get(), &o, &so, ctx, &r, cube.data(), peaks.data()));
+  else
+    ck(xe_search(h.get(), &o, &so, &r, cube.data(), peaks.data(), nullptr));
   Solution s;
   s.backend = "b200";
   s.nodes_explored = r.n_evaluated;

@@ -65,3 +65,66 @@ def exchange_best(obj: float, index: int, n_valid: int, offset: int = 0, device=
     if gkey == NONE:
         return Incumbent(float("inf"), -1, int(v.item()))
     return Incumbent(float(np.int64(gkey).view(np.float64)), int(u.item()), int(v.item()))
+
+
+class NcclContext:
+    """The native multi-GPU context of the C ABI (xe_ctx: device, rank, world,
+    NCCL communicator; csrc/dist.cpp) for C/C++-style callers: rank 0 creates
+    the NCCL id, which the caller distributes (here over torch.distributed
+    when it is initialised).  exchange_best() and search() run the same
+    exchanges as this module's torch.distributed versions, natively."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        import ctypes as C
+        from . import _lib
+        if nccl_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                _lib.check(_lib.LIB.xe_nccl_unique_id(buf))
+            if world > 1:
+                import torch
+                import torch.distributed as dist
+                t = torch.tensor(list(bytes(buf)), dtype=torch.uint8, device="cuda")
+                dist.broadcast(t, src=0)
+                buf = (C.c_uint8 * 128)(*t.cpu().tolist())
+        else:
+            buf = (C.c_uint8 * 128)(*nccl_id)
+        self._h = C.c_void_p()
+        _lib.check(_lib.LIB.xe_ctx_create(device, rank, world, buf, C.byref(self._h)))
+        self.device, self.rank, self.world = device, rank, world
+
+    def close(self):
+        from . import _lib
+        if self._h:
+            _lib.check(_lib.LIB.xe_ctx_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def exchange_best(self, obj: float, index: int, n_valid: int, offset: int = 0) -> Incumbent:
+        import ctypes as C
+        from . import _lib
+        b = _lib.Best(obj, index, n_valid)
+        _lib.check(_lib.LIB.xe_ctx_exchange_best(self._h, offset, C.byref(b)))
+        return Incumbent(b.obj, b.index, b.n_valid)
+
+    def search(self, problem, opts=None, **kw):
+        """xe_search_dist: the search sharded over this context's ranks."""
+        import ctypes as C
+        from . import _lib
+        from .api import ModelOptions
+        so = _lib.SearchOpts()
+        _lib.LIB.xe_search_opts_default(C.byref(so))
+        for k, v in kw.items():
+            setattr(so, k, v)
+        res = _lib.SearchResult()
+        cube = np.zeros(problem.cube_words, np.uint32)
+        peaks = np.zeros(problem.D, np.int64)
+        mo = (opts or ModelOptions()).c()
+        _lib.check(_lib.LIB.xe_search_dist(problem.handle, C.byref(mo), C.byref(so), self._h, C.byref(res),
+                                           cube.ctypes.data, peaks.ctypes.data))
+        return res, cube, peaks
