@@ -207,6 +207,38 @@ def unet_doc(tight_pct=None) -> str:
                              ["cpu", "gpu0", "gpu1", "gpu2"], 4, tight_pct)
 
 
+def forward_doc(direct_text: str, F: int, fwd_edges) -> str:
+    """The same training problem as a "forward" document (the loader's
+    forward-DAG form, loader.cpp expand_training_graph): forward op f with its
+    inputs, output bytes and costs taken from op f of the direct document,
+    its backward from op 2F+1-f; op 0 becomes the document's input."""
+    d = json.loads(direct_text)
+    ops = d["operators"]
+    pars = {f: [] for f in range(1, F + 1)}
+    for (u, v) in fwd_edges:
+        pars[v].append(u)
+    home = [k for k, c in ops[0]["costs_ms"].items() if c == 0.0][0]
+    fwd = []
+    for f in range(1, F + 1):
+        b = ops[2 * F + 1 - f]
+        fwd.append({"name": ops[f]["name"], "inputs": pars[f], "output_bytes": ops[f]["output_bytes"],
+                    "costs_ms": ops[f]["costs_ms"], "backward_output_bytes": b["output_bytes"],
+                    "backward_costs_ms": b["costs_ms"]})
+    out = {"name": d["name"], "devices": d["devices"], "links": d["links"],
+           "input": {"output_bytes": ops[0]["output_bytes"], "home": home}, "forward": fwd}
+    return json.dumps(out)
+
+
+def resnet50_forward_doc(tight_pct=None) -> str:
+    F, fe = resnet50_forward()
+    return forward_doc(resnet50_doc(tight_pct), F, fe)
+
+
+def unet_forward_doc(tight_pct=None) -> str:
+    F, fe = unet_forward()
+    return forward_doc(unet_doc(tight_pct), F, fe)
+
+
 def random2000_doc(tight_pct=None) -> str:
     return _random_costs_doc("random2000", 2000, random_dag_edges(2000, 1),
                              ["cpu"] + [f"gpu{i}" for i in range(7)], 5, tight_pct)

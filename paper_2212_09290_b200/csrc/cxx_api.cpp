@@ -39,6 +39,7 @@
 #include "xengine/schedule.hpp"
 #include "xengine/solver.hpp"
 #include "xengine_b200.h"
+#include "xe_internal.hpp"
 
 namespace xengine {
 
@@ -392,94 +393,6 @@ std::vector<uint32_t> pack_cube(const BitCube& R, const BitCube& S) {
   return c;
 }
 
-// ---- document -> Problem (validation already done by the C loader) -------
-std::vector<double> costs_from(const json& jc, const Problem& p) {
-  std::vector<double> c(static_cast<size_t>(p.device_count()), kProhibitiveMs);
-  for (auto it = jc.begin(); it != jc.end(); ++it) c[static_cast<size_t>(p.find_device(it.key()))] = it.value().get<double>();
-  return c;
-}
-std::pair<int, int> pair_from(const std::string& key, const Problem& p) {
-  const auto at = key.find("->");
-  return {p.find_device(key.substr(0, at)), p.find_device(key.substr(at + 2))};
-}
-CopyLinkModel links_from(const json& doc, const Problem& p) {
-  CopyLinkModel cm;
-  if (!doc.contains("links")) return cm;
-  for (const auto& jl : doc["links"]) {
-    auto end = [&](const char* f) {
-      const std::string s = jl.at(f).get<std::string>();
-      return s == "*" ? -1 : p.find_device(s);
-    };
-    cm.links.push_back({end("from"), end("to"), jl.at("latency_ms").get<double>(), jl.at("bytes_per_ms").get<double>()});
-  }
-  return cm;
-}
-std::vector<DeviceSpec> devices_from(const json& doc) {
-  std::vector<DeviceSpec> out;
-  for (const auto& jd : doc["devices"]) {
-    DeviceSpec d;
-    d.id = jd["id"].get<std::string>();
-    d.budget_bytes = jd["budget_bytes"].get<int64_t>();
-    if (jd.contains("ram_bytes")) d.ram_bytes = jd["ram_bytes"].get<int64_t>();
-    out.push_back(std::move(d));
-  }
-  return out;
-}
-
-Problem problem_from(const json& doc) {
-  Problem p;
-  p.name = doc.value("name", std::string("unnamed"));
-  p.devices = devices_from(doc);
-  if (doc.contains("layers")) {
-    const CopyLinkModel cm = links_from(doc, p);
-    std::vector<LayerSpec> layers;
-    for (const auto& jl : doc["layers"]) {
-      LayerSpec l;
-      l.name = jl.at("name").get<std::string>();
-      l.output_bytes = jl.at("output_bytes").get<int64_t>();
-      l.costs_ms = costs_from(jl.at("costs_ms"), p);
-      l.backward_output_bytes = jl.at("backward_output_bytes").get<int64_t>();
-      l.backward_costs_ms = costs_from(jl.at("backward_costs_ms"), p);
-      layers.push_back(std::move(l));
-    }
-    const json& in = doc["input"];
-    Problem g = make_training_graph(p.name, p.devices, cm, layers, in.at("output_bytes").get<int64_t>(),
-                                    p.find_device(in.at("home").get<std::string>()));
-    if (doc.contains("edge_copy_ms")) {
-      std::map<std::pair<int, int>, double> ov;
-      for (auto it = doc["edge_copy_ms"].begin(); it != doc["edge_copy_ms"].end(); ++it)
-        ov[pair_from(it.key(), g)] = it.value().get<double>();
-      for (auto& e : g.edges) e.override_copy_ms = ov;
-    }
-    return g;
-  }
-  for (const auto& jo : doc["operators"]) {
-    OperatorNode op;
-    op.name = jo["name"].get<std::string>();
-    op.output_bytes = jo["output_bytes"].get<int64_t>();
-    op.costs_ms = costs_from(jo.at("costs_ms"), p);
-    if (jo.contains("pinned")) op.pinned_device = p.find_device(jo["pinned"].get<std::string>());
-    p.operators.push_back(std::move(op));
-  }
-  if (doc.contains("edges"))
-    for (const auto& je : doc["edges"]) {
-      TensorEdge e;
-      if (je.is_array()) {
-        e.src = je[0].get<int>();
-        e.dst = je[1].get<int>();
-      } else {
-        e.src = je.at("src").get<int>();
-        e.dst = je.at("dst").get<int>();
-        if (je.contains("copy_ms"))
-          for (auto it = je["copy_ms"].begin(); it != je["copy_ms"].end(); ++it)
-            e.override_copy_ms[pair_from(it.key(), p)] = it.value().get<double>();
-      }
-      p.edges.push_back(std::move(e));
-    }
-  p.copy_model = links_from(doc, p);
-  return p;
-}
-
 }  // namespace
 
 // ============================ problem.hpp ==================================
@@ -491,14 +404,36 @@ int Problem::find_device(const std::string& id) const {
 }
 
 Problem load_problem(const std::string& json_text) {
-  xe_problem* h = nullptr;  // host-only parse: the reference's validation and error codes
-  ck(xe_problem_parse_json(json_text.c_str(), &h));
-  xe_problem_destroy(h);
+  // the library's one document parser (loader.cpp: the reference's
+  // validation order, messages and error codes), then the value types
+  xe::ParsedDoc d;
   try {
-    return problem_from(json::parse(json_text));
-  } catch (const json::exception& ex) {
-    raise(Errc::MalformedDocument, ex.what());
+    d = xe::parse_problem_document(json_text);
+  } catch (const xe::Error& e) {
+    raise(static_cast<Errc>(e.code - 1), e.what());
   }
+  const xe::HostProblem& h = d.p;
+  Problem p;
+  p.name = d.name;
+  for (int k = 0; k < h.D; ++k) {
+    DeviceSpec ds;
+    ds.id = h.device_ids[static_cast<size_t>(k)];
+    ds.budget_bytes = h.budget[static_cast<size_t>(k)];
+    if (d.ram[static_cast<size_t>(k)] >= 0) ds.ram_bytes = d.ram[static_cast<size_t>(k)];
+    p.devices.push_back(std::move(ds));
+  }
+  for (int i = 0; i < h.T; ++i) {
+    OperatorNode op;
+    op.name = h.op_names[static_cast<size_t>(i)];
+    op.output_bytes = h.mass[static_cast<size_t>(i)];
+    for (int k = 0; k < h.D; ++k) op.costs_ms.push_back(h.cost[static_cast<size_t>(k) * h.T + i]);
+    if (d.pinned[static_cast<size_t>(i)] >= 0) op.pinned_device = d.pinned[static_cast<size_t>(i)];
+    p.operators.push_back(std::move(op));
+  }
+  for (int e = 0; e < h.E; ++e)
+    p.edges.push_back(TensorEdge{h.src[static_cast<size_t>(e)], h.dst[static_cast<size_t>(e)], d.overrides[static_cast<size_t>(e)]});
+  for (const auto& l : d.links) p.copy_model.links.push_back({l.from, l.to, l.latency, l.rate});
+  return p;
 }
 
 Problem load_problem_file(const std::string& path) {
@@ -531,38 +466,31 @@ void validate_problem(const Problem& p) {
 
 Problem make_training_graph(const std::string& name, std::vector<DeviceSpec> devices, CopyLinkModel copy_model,
                             const std::vector<LayerSpec>& layers, std::int64_t input_bytes, int input_home) {
-  const int D = static_cast<int>(devices.size()), L = static_cast<int>(layers.size());
-  if (L == 0) raise(Errc::EmptyNetwork, "training graph needs at least one layer");
-  if (input_bytes <= 0) raise(Errc::NonPositiveSize, "input_bytes must be positive");
-  if (input_home < 0 || input_home >= D) raise(Errc::UnknownDevice, "input home index");
-  auto costs = [&](const std::vector<double>& c, const std::string& what) {
-    if (static_cast<int>(c.size()) != D) raise(Errc::DimensionMismatch, what + " cost vector size");
-    if (std::any_of(c.begin(), c.end(), [](double v) { return v < 0.0; })) raise(Errc::NegativeCost, what + " cost");
-    return c;
-  };
+  // the chain is the forward network k-1 -> k; the library's one expansion
+  // (xe::expand_training_graph) also serves the document loaders
+  std::vector<xe::ForwardOp> fwd;
+  for (size_t k = 0; k < layers.size(); ++k) {
+    const auto& l = layers[k];
+    fwd.push_back({l.name, {static_cast<int>(k)}, l.output_bytes, l.backward_output_bytes, l.costs_ms,
+                   l.backward_costs_ms});
+  }
   Problem p;
   p.name = name;
+  const int D = static_cast<int>(devices.size());
   p.devices = std::move(devices);
   p.copy_model = std::move(copy_model);
-  // op 0: the graph input, a reload on its home device only
-  OperatorNode in{"input", input_bytes, std::vector<double>(static_cast<size_t>(D), kProhibitiveMs), input_home};
-  in.costs_ms[static_cast<size_t>(input_home)] = 0.0;
-  p.operators.push_back(std::move(in));
-  for (const auto& l : layers) {  // forward chain 1..L
-    if (l.output_bytes <= 0) raise(Errc::NonPositiveSize, "layer " + l.name + " output_bytes");
-    p.operators.push_back({l.name, l.output_bytes, costs(l.costs_ms, "layer " + l.name), std::nullopt});
+  std::vector<std::string> names;
+  std::vector<int64_t> bytes;
+  std::vector<std::vector<double>> costs;
+  std::vector<int32_t> src, dst;
+  try {
+    xe::expand_training_graph(D, input_bytes, input_home, fwd, names, bytes, costs, src, dst);
+  } catch (const xe::Error& e) {
+    raise(static_cast<Errc>(e.code - 1), e.what());
   }
-  for (int k = L - 1; k >= 0; --k) {  // backward chain L+1..2L, last layer first
-    const auto& l = layers[static_cast<size_t>(k)];
-    if (l.backward_output_bytes <= 0) raise(Errc::NonPositiveSize, "layer " + l.name + " backward_output_bytes");
-    p.operators.push_back({l.name + "'", l.backward_output_bytes, costs(l.backward_costs_ms, "layer " + l.name + " backward"),
-                           std::nullopt});
-  }
-  for (int k = 0; k < L; ++k) p.edges.push_back(TensorEdge{k, k + 1, {}});
-  for (int j = L + 1; j <= 2 * L; ++j) {
-    p.edges.push_back(TensorEdge{j - 1, j, {}});          // gradient from the op before
-    p.edges.push_back(TensorEdge{2 * L - j, j, {}});      // forward input of the layer at j
-  }
+  for (size_t i = 0; i < names.size(); ++i)
+    p.operators.push_back({names[i], bytes[i], costs[i], i == 0 ? std::optional<int>(input_home) : std::nullopt});
+  for (size_t e = 0; e < src.size(); ++e) p.edges.push_back(TensorEdge{src[e], dst[e], {}});
   validate_problem(p);
   return p;
 }

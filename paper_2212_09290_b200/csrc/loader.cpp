@@ -4,6 +4,8 @@
 // the reference loader (proj/src/problem.cpp):
 //   direct documents          problem.cpp:140-188
 //   layered training graphs   problem.cpp:190-224, make_training_graph 280-338
+//   forward-DAG documents      make_training_graph generalised to a forward
+//                              DAG ("forward" key)
 //   structural validation     problem.cpp:254-278
 //   copy_cost resolution      problem.cpp:358-380 (override > most specific link)
 //   energy section            proj/src/model.cpp:314-367
@@ -12,6 +14,7 @@
 
 #include <json.hpp>
 
+#include <algorithm>
 #include <cmath>
 #include <set>
 
@@ -23,16 +26,8 @@ namespace {
 using nlohmann::json;
 constexpr double kProhibitive = 1.0e9;  // problem.hpp:16
 
-struct Link {
-  int from, to;
-  double latency, rate;
-};
-
-struct Doc {
-  HostProblem p;
-  std::vector<Link> links;
-  std::vector<std::map<std::pair<int, int>, double>> overrides;  // per edge
-};
+using Link = DocLink;
+using Doc = ParsedDoc;
 
 int64_t positive_int(const json& j, const std::string& what) {
   if (!j.is_number_integer()) fail(XE_ERR_MALFORMED_DOCUMENT, what + " must be an integer byte count");
@@ -54,7 +49,7 @@ int device_index(const HostProblem& p, const std::string& id) {
   return -1;
 }
 
-void read_devices(const json& doc, HostProblem& p) {
+void read_devices(const json& doc, HostProblem& p, std::vector<int64_t>* ram_out) {
   if (!doc.contains("devices") || !doc["devices"].is_array() || doc["devices"].empty())
     fail(XE_ERR_MALFORMED_DOCUMENT, "document needs a non-empty devices array");
   std::set<std::string> ids;
@@ -64,12 +59,14 @@ void read_devices(const json& doc, HostProblem& p) {
     std::string id = jd["id"].get<std::string>();
     if (!ids.insert(id).second) fail(XE_ERR_MALFORMED_DOCUMENT, "duplicate device id " + id);
     int64_t budget = positive_int(jd.at("budget_bytes"), "device " + id + " budget_bytes");
+    int64_t ram = -1;
     if (jd.contains("ram_bytes")) {
-      int64_t ram = positive_int(jd["ram_bytes"], "device " + id + " ram_bytes");
+      ram = positive_int(jd["ram_bytes"], "device " + id + " ram_bytes");
       if (ram < budget) fail(XE_ERR_MALFORMED_DOCUMENT, "device " + id + " budget exceeds its ram");
     }
     p.device_ids.push_back(id);
     p.budget.push_back(budget);
+    if (ram_out) ram_out->push_back(ram);
   }
   p.D = static_cast<int>(p.device_ids.size());
 }
@@ -142,7 +139,7 @@ void finish_costs(HostProblem& p, const std::vector<std::vector<double>>& costs)
 Doc read_direct(const json& doc) {
   Doc out;
   HostProblem& p = out.p;
-  read_devices(doc, p);
+  read_devices(doc, p, &out.ram);
   if (!doc.contains("operators") || !doc["operators"].is_array() || doc["operators"].empty())
     fail(XE_ERR_EMPTY_NETWORK, "document has no operators");
   std::vector<std::vector<double>> costs;
@@ -152,8 +149,12 @@ Doc read_direct(const json& doc) {
     std::string name = jo["name"].get<std::string>();
     int64_t bytes = positive_int(jo.at("output_bytes"), "operator " + name + " output_bytes");
     auto c = read_costs(jo.at("costs_ms"), p, "operator " + name);
-    if (jo.contains("pinned") && device_index(p, jo["pinned"].get<std::string>()) < 0)
-      fail(XE_ERR_UNKNOWN_DEVICE, "operator " + name + " pinned to unknown device");
+    int pin = -1;
+    if (jo.contains("pinned")) {
+      pin = device_index(p, jo["pinned"].get<std::string>());
+      if (pin < 0) fail(XE_ERR_UNKNOWN_DEVICE, "operator " + name + " pinned to unknown device");
+    }
+    out.pinned.push_back(pin);
     add_op(p, name, bytes, c, costs);
   }
   finish_costs(p, costs);
@@ -187,56 +188,53 @@ Doc read_direct(const json& doc) {
   return out;
 }
 
-// 2L+1 operators: input, forward chain, backward chain in reverse layer
-// order; L chain edges, then per backward op the gradient edge and the
-// saved-tensor edge (the input for the first layer).
-Doc read_layered(const json& doc) {
+// The training-graph documents: "layers" (the reference's chain form,
+// problem.cpp:190-224) and "forward" (a forward DAG: each op lists its
+// inputs) expand through expand_training_graph.
+Doc read_training(const json& doc, bool chain) {
   Doc out;
   HostProblem& p = out.p;
-  read_devices(doc, p);
+  read_devices(doc, p, &out.ram);
   out.links = read_links(doc, p);
   if (!doc.contains("input") || !doc["input"].is_object())
     fail(XE_ERR_MALFORMED_DOCUMENT, "layer document needs an input object");
   int64_t in_bytes = positive_int(doc["input"].at("output_bytes"), "input output_bytes");
   int home = device_index(p, doc["input"].at("home").get<std::string>());
   if (home < 0) fail(XE_ERR_UNKNOWN_DEVICE, "input home device");
-
-  struct Layer {
-    std::string name;
-    int64_t out, bout;
-    std::vector<double> c, bc;
-  };
-  std::vector<Layer> layers;
-  for (const auto& jl : doc["layers"]) {
-    Layer l;
+  std::vector<ForwardOp> fwd;
+  const json& list = chain ? doc["layers"] : doc["forward"];
+  if (!list.is_array()) fail(XE_ERR_MALFORMED_DOCUMENT, chain ? "layers must be an array" : "forward must be an array");
+  for (const auto& jl : list) {
+    ForwardOp l;
     l.name = jl.at("name").get<std::string>();
-    l.out = positive_int(jl.at("output_bytes"), "layer " + l.name + " output_bytes");
-    l.c = read_costs(jl.at("costs_ms"), p, "layer " + l.name);
-    l.bout = positive_int(jl.at("backward_output_bytes"), "layer " + l.name + " backward_output_bytes");
-    l.bc = read_costs(jl.at("backward_costs_ms"), p, "layer " + l.name + " backward");
-    layers.push_back(std::move(l));
+    l.bytes = positive_int(jl.at("output_bytes"), "layer " + l.name + " output_bytes");
+    l.costs = read_costs(jl.at("costs_ms"), p, "layer " + l.name);
+    l.bwd_bytes = positive_int(jl.at("backward_output_bytes"), "layer " + l.name + " backward_output_bytes");
+    l.bwd_costs = read_costs(jl.at("backward_costs_ms"), p, "layer " + l.name + " backward");
+    const int k = static_cast<int>(fwd.size()) + 1;
+    if (chain) {
+      l.inputs = {k - 1};
+    } else {
+      if (!jl.contains("inputs") || !jl["inputs"].is_array() || jl["inputs"].empty())
+        fail(XE_ERR_MALFORMED_DOCUMENT, "forward op " + l.name + " needs a non-empty inputs array");
+      for (const auto& ji : jl["inputs"]) {
+        if (!ji.is_number_integer()) fail(XE_ERR_MALFORMED_DOCUMENT, "forward op " + l.name + " inputs are op indices");
+        const int u = ji.get<int>();
+        if (u < 0 || u >= k)
+          fail(XE_ERR_NON_TOPOLOGICAL_EDGE, "forward op " + l.name + " input " + std::to_string(u) + " is not earlier");
+        l.inputs.push_back(u);
+      }
+    }
+    fwd.push_back(std::move(l));
   }
-  if (layers.empty()) fail(XE_ERR_EMPTY_NETWORK, "training graph needs at least one layer");
-  const int L = static_cast<int>(layers.size());
+  if (fwd.empty()) fail(XE_ERR_EMPTY_NETWORK, "training graph needs at least one layer");
   std::vector<std::vector<double>> costs;
-  std::vector<double> cin(static_cast<size_t>(p.D), kProhibitive);
-  cin[static_cast<size_t>(home)] = 0.0;
-  add_op(p, "input", in_bytes, cin, costs);
-  for (int k = 0; k < L; ++k) add_op(p, layers[static_cast<size_t>(k)].name, layers[static_cast<size_t>(k)].out, layers[static_cast<size_t>(k)].c, costs);
-  for (int k = L - 1; k >= 0; --k)
-    add_op(p, layers[static_cast<size_t>(k)].name + "'", layers[static_cast<size_t>(k)].bout, layers[static_cast<size_t>(k)].bc, costs);
+  std::vector<int64_t> bytes;
+  expand_training_graph(p.D, in_bytes, home, fwd, p.op_names, bytes, costs, p.src, p.dst);
+  p.mass = bytes;
   finish_costs(p, costs);
-  for (int k = 0; k < L; ++k) {
-    p.src.push_back(k);
-    p.dst.push_back(k + 1);
-  }
-  for (int j = L + 1; j <= 2 * L; ++j) {
-    int layer = 2 * L + 1 - j;
-    p.src.push_back(j - 1);  // upstream gradient
-    p.dst.push_back(j);
-    p.src.push_back(layer - 1);  // saved forward tensor
-    p.dst.push_back(j);
-  }
+  out.pinned.assign(static_cast<size_t>(p.T), -1);
+  out.pinned[0] = home;
   p.E = static_cast<int>(p.src.size());
   validate(p);
   std::map<std::pair<int, int>, double> ov;
@@ -356,7 +354,66 @@ void validate(const HostProblem& p) {
       fail(XE_ERR_MALFORMED_DOCUMENT, "operator " + std::to_string(v) + " has no incoming edge; only operator 0 is a source");
 }
 
-HostProblem load_problem_json(const std::string& text) {
+void expand_training_graph(int D, int64_t input_bytes, int input_home, const std::vector<ForwardOp>& fwd,
+                           std::vector<std::string>& names, std::vector<int64_t>& bytes,
+                           std::vector<std::vector<double>>& costs, std::vector<int32_t>& src,
+                           std::vector<int32_t>& dst) {
+  if (fwd.empty()) fail(XE_ERR_EMPTY_NETWORK, "training graph needs at least one layer");
+  if (input_bytes <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "input_bytes must be positive");
+  if (input_home < 0 || input_home >= D) fail(XE_ERR_UNKNOWN_DEVICE, "input home index");
+  const int F = static_cast<int>(fwd.size());
+  auto checked = [&](const std::vector<double>& c, const std::string& ctx) {
+    if (static_cast<int>(c.size()) != D) fail(XE_ERR_DIMENSION_MISMATCH, ctx + " cost vector size");
+    for (double v : c)
+      if (v < 0.0) fail(XE_ERR_NEGATIVE_COST, ctx + " cost");
+    return c;
+  };
+  names.assign(1, "input");
+  bytes.assign(1, input_bytes);
+  costs.assign(1, std::vector<double>(static_cast<size_t>(D), kProhibitive));
+  costs[0][static_cast<size_t>(input_home)] = 0.0;  // a reload, not a computation
+  for (const auto& l : fwd) {
+    if (l.bytes <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "layer " + l.name + " output_bytes");
+    names.push_back(l.name);
+    bytes.push_back(l.bytes);
+    costs.push_back(checked(l.costs, "layer " + l.name));
+  }
+  for (int f = F; f >= 1; --f) {
+    const auto& l = fwd[static_cast<size_t>(f - 1)];
+    if (l.bwd_bytes <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "layer " + l.name + " backward_output_bytes");
+    names.push_back(l.name + "'");
+    bytes.push_back(l.bwd_bytes);
+    costs.push_back(checked(l.bwd_costs, "layer " + l.name + " backward"));
+  }
+  std::vector<std::vector<int>> cons(static_cast<size_t>(F) + 1);
+  src.clear();
+  dst.clear();
+  for (int f = 1; f <= F; ++f)  // forward edges
+    for (int u : fwd[static_cast<size_t>(f - 1)].inputs) {
+      src.push_back(u);
+      dst.push_back(f);
+      cons[static_cast<size_t>(u)].push_back(f);
+    }
+  for (auto& c : cons) std::sort(c.begin(), c.end());
+  for (int j = F + 1; j <= 2 * F; ++j) {
+    const int f = 2 * F + 1 - j;  // the forward op whose backward sits at j
+    if (cons[static_cast<size_t>(f)].empty()) {
+      src.push_back(F);  // upstream gradient of the loss
+      dst.push_back(j);
+    } else {
+      for (int c : cons[static_cast<size_t>(f)]) {
+        src.push_back(2 * F + 1 - c);  // upstream gradient from the consumer's backward
+        dst.push_back(j);
+      }
+    }
+    for (int u : fwd[static_cast<size_t>(f - 1)].inputs) {  // saved forward tensors
+      src.push_back(u);
+      dst.push_back(j);
+    }
+  }
+}
+
+ParsedDoc parse_problem_document(const std::string& text) {
   json doc;
   try {
     doc = json::parse(text);
@@ -365,13 +422,25 @@ HostProblem load_problem_json(const std::string& text) {
   }
   if (!doc.is_object()) fail(XE_ERR_MALFORMED_DOCUMENT, "top level must be an object");
   try {
-    Doc d = doc.contains("layers") ? read_layered(doc) : read_direct(doc);
-    resolve_copies(d);
-    read_energy(doc, d.p);
-    return d.p;
+    Doc d = doc.contains("layers")    ? read_training(doc, true)
+            : doc.contains("forward") ? read_training(doc, false)
+                                      : read_direct(doc);
+    d.name = doc.value("name", std::string("unnamed"));
+    return d;
   } catch (const json::exception& ex) {
     fail(XE_ERR_MALFORMED_DOCUMENT, ex.what());
   }
+}
+
+HostProblem load_problem_json(const std::string& text) {
+  Doc d = parse_problem_document(text);
+  resolve_copies(d);
+  try {
+    read_energy(json::parse(text), d.p);
+  } catch (const json::exception& ex) {
+    fail(XE_ERR_MALFORMED_DOCUMENT, ex.what());
+  }
+  return d.p;
 }
 
 }  // namespace xe

@@ -110,6 +110,41 @@ struct HostProblem {
 HostProblem load_problem_json(const std::string& text);  // loader.cpp
 void validate(const HostProblem& p);                      // loader.cpp
 
+// The parsed, validated document before copy-cost resolution: what the C++
+// API's Problem holds (one JSON parser serves the C ABI and the C++ API).
+struct DocLink {
+  int from, to;  // -1 = any device
+  double latency, rate;
+};
+struct ParsedDoc {
+  std::string name;
+  HostProblem p;  // devices, operators, edges (copies unresolved, no energy)
+  std::vector<int64_t> ram;      // [D], -1 = absent
+  std::vector<int32_t> pinned;   // [T], -1 = none
+  std::vector<DocLink> links;
+  std::vector<std::map<std::pair<int, int>, double>> overrides;  // per edge
+};
+ParsedDoc parse_problem_document(const std::string& text);  // loader.cpp
+
+// Forward network -> training graph (make_training_graph, problem.cpp:280-338,
+// generalised from a layer chain to a forward DAG): op 0 = the input
+// (prohibitive cost except on its home device), forward ops 1..F, the
+// backward of forward op f at 2F+1-f.  Edges: forward edges (u -> f, inputs
+// in listed order, f ascending), then per backward op j (ascending) the
+// upstream gradients (from the backward of each consumer of f, ascending;
+// from the last forward op when f has none) and the saved tensors (f's
+// inputs in listed order).  On a chain this is the reference's edge order.
+struct ForwardOp {
+  std::string name;
+  std::vector<int> inputs;  // 0 = the input tensor, k = forward op k (k < this op's index)
+  int64_t bytes, bwd_bytes;
+  std::vector<double> costs, bwd_costs;  // [D]
+};
+void expand_training_graph(int D, int64_t input_bytes, int input_home, const std::vector<ForwardOp>& fwd,
+                           std::vector<std::string>& names, std::vector<int64_t>& bytes,
+                           std::vector<std::vector<double>>& costs, std::vector<int32_t>& src,
+                           std::vector<int32_t>& dst);  // loader.cpp
+
 // Kernel-side problem image: all pointers are device pointers.  Built once
 // per handle (problem.cu) and passed by value to kernels.
 struct DevProblem {
