@@ -15,6 +15,7 @@
 //   when every objective term is dyadic (exact_fix_k >= 0): then both orders
 //   give the same bits.
 
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 
@@ -192,6 +193,12 @@ void il_to_canon_device(const xe_problem* pr, const uint64_t* il, int64_t first,
   XE_CUDA(cudaGetLastError());
 }
 
+// XE_STREAM_WIDE=0 keeps the 8-warp plan everywhere (A/B switch)
+static bool wide_disabled() {
+  const char* e = std::getenv("XE_STREAM_WIDE");
+  return e && e[0] == '0';
+}
+
 bool stream_supported(const xe_problem* pr, const xe_model_opts& opts) {
   const HostProblem& h = pr->h;
   if (opts.use_energy && h.has_energy) return false;  // energy terms/rows: the exact kernels
@@ -224,33 +231,46 @@ int eval_stream_device(const xe_problem* pr, const xe_model_opts& opts, const ui
   const int msz = m32 ? 4 : 8;
   const int NW = il_words(h.T);
   const int maxd = h.D <= 4 ? h.D : 8;
-  int off = 0;
-  auto take = [&](int bytes) {
-    int o = off;
-    off = align16(off + bytes);
-    return o;
-  };
-  take(8 * NW * 256 * msz);  // byte tables at offset 0
-  a.off_mass = take(msz * h.T);
-  a.off_pmask = take(8 * h.T * NW);
-  a.off_cons = take(8 * h.T * NW);
-  a.off_c = take(8 * h.D * h.T);
-  a.off_w = take(8 * std::max(1, h.E * h.D * h.D));
-  a.off_inl = take(4 * std::max(1, h.E));
-  a.off_inptr = take(4 * (h.T + 1));
-  a.off_inedge = take(4 * std::max(1, h.E));
-  a.off_src = take(4 * std::max(1, h.E));
-  a.off_dst = take(4 * std::max(1, h.E));
-  a.off_warp = off;
-  // per warp: queue | fl[32] | cnt[32] | pk[32][maxd] | slow[32] | park[32]
-  const int park_bytes = 8 + 16 + 3 * 8 * maxd * NW + msz * maxd + 4;
-  const int park_sz = (park_bytes + 7) & ~7;
-  a.warp_bytes = align16(static_cast<int>(sizeof(Job)) * kQCap + 4 * 32 + 4 * 32 + msz * 32 * maxd +
-                         8 * 32 + 32 * park_sz + 64);
-  a.smem_bytes = off + kWarps * a.warp_bytes;
   int nsm = 0, smem_limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
   XE_CUDA(cudaDeviceGetAttribute(&smem_limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
+  // the wide plan (one 24-warp CTA per SM, 11-bit mass tables): one-word
+  // rows of 34..64 operators with int32 masses and D in 2..4, when its
+  // shared-memory plan fits; else the 8-warp plan
+  const int nch = (h.T + 10) / 11;
+  auto plan = [&](bool wide) {
+    int off = 0;
+    auto take = [&](int bytes) {
+      int o = off;
+      off = align16(off + bytes);
+      return o;
+    };
+    take(wide ? nch * 2048 * msz : 8 * NW * 256 * msz);  // mass tables at offset 0
+    a.off_mass = take(msz * h.T);
+    a.off_pmask = take(8 * h.T * NW);
+    a.off_cons = take(8 * h.T * NW);
+    a.off_c = take(8 * h.D * h.T);
+    a.off_w = take(8 * std::max(1, h.E * h.D * h.D));
+    a.off_inl = take(4 * std::max(1, h.E));
+    a.off_inptr = take(4 * (h.T + 1));
+    a.off_inedge = take(4 * std::max(1, h.E));
+    a.off_src = take(4 * std::max(1, h.E));
+    a.off_dst = take(4 * std::max(1, h.E));
+    a.off_warp = off;
+    // per warp: queue | fl[32] | cnt[32] | pk[32][maxd] | slow[32] | park[32]
+    const int park_bytes = 8 + 16 + 3 * 8 * maxd * NW + msz * maxd + 4;
+    const int park_sz = (park_bytes + 7) & ~7;
+    a.warp_bytes = align16(static_cast<int>(sizeof(Job)) * kQCap + 4 * 32 + 4 * 32 + msz * 32 * maxd +
+                           8 * 32 + 32 * park_sz + 64);
+    a.smem_bytes = off + (wide ? kWideWarps : kWarps) * a.warp_bytes;
+  };
+  bool wide = NW == 1 && m32 && h.D >= 2 && h.D <= 4 && nch >= 4 && !wide_disabled();
+  if (wide) {
+    plan(true);
+    if (a.smem_bytes > smem_limit) wide = false;
+  }
+  if (!wide) plan(false);
+  const int warps = wide ? kWideWarps : kWarps;
   if (a.smem_bytes > smem_limit) fail(XE_ERR_TOO_LARGE, "streaming evaluator: shared-memory plan too large");
   const size_t nw_max = static_cast<size_t>(nsm) * 8 * cube::kWarps;  // eval_scratch_bytes layout
   a.wbest_key = reinterpret_cast<uint64_t*>(scratch);
@@ -261,16 +281,16 @@ int eval_stream_device(const xe_problem* pr, const xe_model_opts& opts, const ui
     const int tl = h.T - 64 * (NW - 1);
     const int nbl = (tl + 7) / 8;
     switch (NW) {
-      case 1: grid = launch_stream<1>(a, m32, nbl, stream, nsm); break;
-      case 2: grid = launch_stream<2>(a, m32, nbl, stream, nsm); break;
-      case 3: grid = launch_stream<3>(a, m32, nbl, stream, nsm); break;
-      default: grid = launch_stream<4>(a, m32, nbl, stream, nsm); break;
+      case 1: grid = launch_stream<1>(a, m32, wide ? nch : nbl, stream, nsm, wide); break;
+      case 2: grid = launch_stream<2>(a, m32, wide ? nch : nbl, stream, nsm, wide); break;
+      case 3: grid = launch_stream<3>(a, m32, wide ? nch : nbl, stream, nsm, wide); break;
+      default: grid = launch_stream<4>(a, m32, nbl, stream, nsm, false); break;
     }
-    if (static_cast<size_t>(grid) * kWarps > nw_max) fail(XE_ERR_ARG, "evaluator scratch too small");
+    if (static_cast<size_t>(grid) * warps > nw_max) fail(XE_ERR_ARG, "evaluator scratch too small");
   }
   if (best3) {
     if (n > 0) {
-      reduce_best_launch(a.wbest_key, a.wbest_idx, a.wvalid, grid * kWarps, best3, stream);
+      reduce_best_launch(a.wbest_key, a.wbest_idx, a.wvalid, grid * warps, best3, stream);
     } else {
       const uint64_t none[3] = {~0ull, ~0ull, 0ull};
       XE_CUDA(cudaMemcpyAsync(best3, none, sizeof none, cudaMemcpyHostToDevice, stream));

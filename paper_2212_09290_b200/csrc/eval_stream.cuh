@@ -273,16 +273,23 @@ struct Park {
 // M: integer type of masses and memory sums (int32 when twice the save-all
 // total fits).
 // NBL: bytes of the last bit-row word that carry operators (4, 6 or 8).
-template <int MAXD, int NW, class M, int NBL>
-__global__ void __launch_bounds__(kWarps * 32, (MAXD * NW <= 2) ? 3 : 2)
+//
+// WARPS / TB: the default plan is 8-warp CTAs (2-3 per SM) with one 256-entry
+// mass table per byte of a bit row; the wide plan (T <= 64) is one 24-warp
+// CTA per SM whose 2048-entry tables cover 11 bits each (TB = 11, NBL = the
+// number of 11-bit chunks): the tables are shared by 3x the warps and a row
+// takes 4 lookups instead of 6 at T = 43.
+template <int MAXD, int NW, class M, int NBL, int WARPS = kWarps, int TB = 8>
+__global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2) ? 3 : 2) : 1)
     stream_kernel(const __grid_constant__ StArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const DevProblem& P = a.P;
   const int D = cube::ndev<MAXD>(P), T = P.T, E = P.E;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NBT = 8 * NW;  // byte tables (zero beyond the problem's bytes)
+  static_assert(TB == 8 || (TB == 11 && NW == 1), "11-bit mass tables cover one-word rows");
 
-  M* s_mtab = reinterpret_cast<M*>(smem);  // [NBT][256]
+  M* s_mtab = reinterpret_cast<M*>(smem);  // [NBT][256] or [NBL][2048]
   M* s_mass = reinterpret_cast<M*>(smem + a.off_mass);
   uint64_t* s_pmask = reinterpret_cast<uint64_t*>(smem + a.off_pmask);
   uint64_t* s_cons = reinterpret_cast<uint64_t*>(smem + a.off_cons);
@@ -294,8 +301,18 @@ __global__ void __launch_bounds__(kWarps * 32, (MAXD * NW <= 2) ? 3 : 2)
   int32_t* s_src = reinterpret_cast<int32_t*>(smem + a.off_src);
   int32_t* s_dst = reinterpret_cast<int32_t*>(smem + a.off_dst);
   const int n_dt = D * T, n_copy = E * D * D;
-  for (int i = threadIdx.x; i < NBT * 256; i += blockDim.x)
-    s_mtab[i] = i < P.NB * 256 ? static_cast<M>(P.mtab[i]) : M(0);
+  if (TB == 8) {
+    for (int i = threadIdx.x; i < NBT * 256; i += blockDim.x)
+      s_mtab[i] = i < P.NB * 256 ? static_cast<M>(P.mtab[i]) : M(0);
+  } else {  // chunk c, entry v: the masses of the set bits of v at operators 11c..11c+10
+    for (int i = threadIdx.x; i < NBL * 2048; i += blockDim.x) {
+      const int c = i >> 11, v = i & 2047;
+      M m = 0;
+      for (int b = 0; b < 11; ++b)
+        if (((v >> b) & 1) && 11 * c + b < T) m += static_cast<M>(P.mass[11 * c + b]);
+      s_mtab[i] = m;
+    }
+  }
   for (int i = threadIdx.x; i < T; i += blockDim.x) s_mass[i] = static_cast<M>(P.mass[i]);
   for (int i = threadIdx.x; i < T * NW; i += blockDim.x) {
     s_pmask[i] = P.pmask[i];
@@ -325,8 +342,8 @@ __global__ void __launch_bounds__(kWarps * 32, (MAXD * NW <= 2) ? 3 : 2)
   __syncthreads();
   const Sm<M> sm{s_mtab, s_mass, s_pmask, s_cons, s_c, s_w, s_inptr, s_inedge, s_src, s_dst, s_fl, s_cnt, s_pk};
 
-  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * WARPS + wid;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * WARPS;
   const int64_t ngroups = (a.n + 31) / 32;
   const int64_t K = 2ll * D * T * NW;
   const int dstride = T * NW * 32;  // words between (which,d) blocks
@@ -441,10 +458,16 @@ __global__ void __launch_bounds__(kWarps * 32, (MAXD * NW <= 2) ? 3 : 2)
           Zp[d][j] = z;
           zany[j] |= z;
           // mass of the saved tensors through the byte tables
-          const uint32_t lo = static_cast<uint32_t>(s), hi = static_cast<uint32_t>(s >> 32);
+          if (TB == 8) {
+            const uint32_t lo = static_cast<uint32_t>(s), hi = static_cast<uint32_t>(s >> 32);
 #pragma unroll
-          for (int b = 0; b < (j == NW - 1 ? NBL : 8); ++b)
-            base[d] += s_mtab[(8 * j + b) * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+            for (int b = 0; b < (j == NW - 1 ? NBL : 8); ++b)
+              base[d] += s_mtab[(8 * j + b) * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+          } else {
+#pragma unroll
+            for (int c = 0; c < NBL; ++c)
+              base[d] += s_mtab[c * 2048 + static_cast<int>((s >> (11 * c)) & 0x7ffull)];
+          }
         }
       }
       const bool fast = off == 0 && cnt == 1;
@@ -603,9 +626,14 @@ __global__ void __launch_bounds__(kWarps * 32, (MAXD * NW <= 2) ? 3 : 2)
   }
 }
 
-// launcher instantiated per NW (eval_stream_nw*.cu)
+// launcher instantiated per NW (eval_stream_nw*.cu); wide: the 24-warp,
+// 11-bit-table plan (NW = 1, int32 masses), nbl = its chunk count
 template <int NW>
-int launch_stream(const StArgs& a, bool m32, int nbl, cudaStream_t s, int nsm);
+int launch_stream(const StArgs& a, bool m32, int nbl, cudaStream_t s, int nsm, bool wide);
+#ifndef XE_WIDE_WARPS
+#define XE_WIDE_WARPS 24
+#endif
+constexpr int kWideWarps = XE_WIDE_WARPS;
 
 }  // namespace st
 }  // namespace xe

@@ -31,7 +31,7 @@ static int launch_nbl(const StArgs& a, bool m32, cudaStream_t s, int nsm) {
 }
 
 template <>
-int launch_stream<2>(const StArgs& a, bool m32, int nbl, cudaStream_t s, int nsm) {
+int launch_stream<2>(const StArgs& a, bool m32, int nbl, cudaStream_t s, int nsm, bool) {
   return nbl <= 4 ? launch_nbl<4>(a, m32, s, nsm) : nbl <= 6 ? launch_nbl<6>(a, m32, s, nsm) : launch_nbl<8>(a, m32, s, nsm);
 }
 
