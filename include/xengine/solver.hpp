@@ -67,6 +67,8 @@ struct SearchParams {
   int max_moves = 4;
   int stall = 15;
   SearchLimits limits;      // time_limit_ms honoured (node_limit: candidates are not nodes)
+  bool exact_polish = true; // D*T <= 64: solve_exact bounded by the search's objective (proof + tail_less winner)
+  std::int64_t exact_polish_ms = 5000;
 };
 
 // Best schedule by the GPU search: K1 model -> K3 LP relaxation -> K4

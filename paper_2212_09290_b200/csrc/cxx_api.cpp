@@ -828,6 +828,85 @@ std::string write_mps(const MilpModel& m) {
   return s;
 }
 
+// The solution side of the external-solver bridge (mps_io.cpp:201-263):
+// "<var> <value>" and CBC's "<idx> <var> <value> <cost>" lines, "# objective"
+// comments and banners; binaries rounded within 1e-4.
+namespace {
+bool sol_is_number(const std::string& t) {
+  if (t.empty()) return false;
+  char* end = nullptr;
+  std::strtod(t.c_str(), &end);
+  return end == t.c_str() + t.size();
+}
+bool sol_is_integer(const std::string& t) {
+  if (t.empty()) return false;
+  size_t i = t[0] == '-' || t[0] == '+' ? 1 : 0;
+  if (i == t.size()) return false;
+  for (; i < t.size(); ++i)
+    if (!std::isdigit(static_cast<unsigned char>(t[i]))) return false;
+  return true;
+}
+std::string sol_lower(std::string t) {
+  for (char& c : t) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  return t;
+}
+}  // namespace
+
+Assignment parse_solution(const std::string& text, const MilpModel& m) {
+  Assignment a;
+  bool any_var = false;
+  auto record = [&](const std::string& name, double value) -> bool {
+    auto ref = parse_var_name(name);
+    if (!ref) return false;  // a banner word, not a variable
+    if (!m.in_space(*ref)) raise(Errc::UnknownVariable, name);
+    if (m.is_binary(ref->family)) {
+      if (std::abs(value) <= 1e-4)
+        value = 0.0;
+      else if (std::abs(value - 1.0) <= 1e-4)
+        value = 1.0;
+      else
+        raise(Errc::NonIntegralBinary, name + " = " + format_number(value));
+    }
+    a.set(*ref, value);
+    any_var = true;
+    return true;
+  };
+  std::istringstream in(text);
+  std::string line;
+  while (std::getline(in, line)) {
+    std::istringstream ls(line);
+    std::vector<std::string> tok;
+    for (std::string t; ls >> t;) tok.push_back(t);
+    if (tok.empty()) continue;
+    if (tok[0][0] == '#') {
+      if (tok.size() >= 3 && tok[0] == "#" && sol_lower(tok[1]) == "objective" && sol_is_number(tok[2]))
+        a.objective_reported = std::strtod(tok[2].c_str(), nullptr);
+      continue;
+    }
+    const std::string low = sol_lower(line);
+    if (low.find("infeasible") != std::string::npos) raise(Errc::InfeasibleMarker, line);
+    if (tok.size() == 2 && sol_is_number(tok[1]) && record(tok[0], std::strtod(tok[1].c_str(), nullptr))) continue;
+    if (tok.size() == 4 && sol_is_integer(tok[0]) && sol_is_number(tok[2]) &&
+        record(tok[1], std::strtod(tok[2].c_str(), nullptr)))
+      continue;
+    if (low.find("objective") != std::string::npos)
+      for (auto it = tok.rbegin(); it != tok.rend(); ++it)
+        if (sol_is_number(*it)) {
+          a.objective_reported = std::strtod(it->c_str(), nullptr);
+          break;
+        }
+  }
+  if (!any_var) raise(Errc::EmptySolution, "no variable lines");
+  return a;
+}
+
+std::string format_solution(const Assignment& a) {
+  std::string out;
+  if (a.objective_reported) out += "# objective " + format_number(*a.objective_reported) + "\n";
+  for (const auto& [ref, val] : a.values) out += var_name(ref) + " " + format_number(val) + "\n";
+  return out;
+}
+
 // ============================ solver.hpp ===================================
 
 Assignment save_all_assignment(const Problem& p, const std::vector<int>& devices) {
@@ -968,6 +1047,29 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
                       r.objective <= r.lp_bound + so.lp_tol * std::max(1.0, std::fabs(r.objective));
   s.status = proven ? SolveStatus::Optimal : SolveStatus::LimitReached;
   s.objective_ms = r.objective;
+  // exact polish (D*T <= 64): solve_exact bounded by the search's objective
+  // proves optimality and returns the reference's tail_less winner among the
+  // optima (solver.cpp:87-92), kept when it is valid under the search's mask
+  if (params.exact_polish && D * T <= 64 && !ctx) {
+    xe_exact_opts eo;
+    xe_exact_opts_default(&eo);
+    eo.upper_bound = r.objective;
+    eo.time_limit_ms = params.exact_polish_ms;
+    xe_exact_result er{};
+    std::vector<uint32_t> ecube(cube.size());
+    ck(xe_solve_exact(h.get(), &o, &eo, &er, ecube.data(), nullptr));
+    if (er.status == 0 && er.found && er.objective <= r.objective) {
+      xe_best b{};
+      ck(xe_eval_cubes_host(h.get(), &o, ecube.data(), 1, nullptr, so.valid_mask, &b));
+      if (b.index == 0) {  // valid under the search's mask
+        cube = ecube;
+        s.objective_ms = b.obj;
+        s.status = SolveStatus::Optimal;
+      } else if (er.objective == r.objective) {
+        s.status = SolveStatus::Optimal;  // the search's schedule attains the proven optimum
+      }
+    }
+  }
   BitCube R(D, T), S(D, T);
   const int W = (T + 31) / 32;
   for (int which = 0; which < 2; ++which)
@@ -977,7 +1079,7 @@ Solution solve_search(const Problem& p, const ModelOptions& opts, const SearchPa
           if ((cube[((static_cast<size_t>(which) * D + d) * T + t) * W + i / 32] >> (i % 32)) & 1u)
             (which ? S : R).at(d, t, i) = 1;
   s.assignment = complete_assignment(p, opts, R, S);
-  s.assignment.objective_reported = r.objective;
+  s.assignment.objective_reported = s.objective_ms;
   return s;
 }
 

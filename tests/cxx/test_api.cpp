@@ -479,6 +479,42 @@ void device_cases() {
     CHECK_THROWS_CODE(assignment_oracle(long_chain(23, 2)), Errc::TooLarge);
     CHECK(assignment_oracle(long_chain(23, 1)).status == SolveStatus::Optimal);
   });
+  // ---- mps_io.hpp parse_solution / format_solution: proj/tests/test_mps_io.cpp:205-286
+  run("parse_solution accepts both solver layouts", [] {
+    MilpModel m = build_model(fixture("chain3"));
+    Assignment a = parse_solution("R_0_0_0 1\nU_0_0_0 4194304\n", m);
+    CHECK(a.at(var_r(0, 0, 0)) == 1.0);
+    CHECK(a.at(var_u(0, 0, 0)) == 4194304.0);
+    CHECK(a.at(var_r(0, 1, 1)) == 0.0);
+    CHECK(!a.objective_reported.has_value());
+    Assignment b = parse_solution(
+        "Optimal - objective value 9.00000000\n      0 R_0_0_0               1                       2\n"
+        "      5 U_0_0_0         4194304                       0\n", m);
+    CHECK(b.at(var_r(0, 0, 0)) == 1.0 && b.at(var_u(0, 0, 0)) == 4194304.0);
+    CHECK(b.objective_reported.has_value() && *b.objective_reported == 9.0);
+    Assignment c = parse_solution("# objective 9.5\nR_0_0_0 1\n", m);
+    CHECK(c.objective_reported.has_value() && *c.objective_reported == 9.5);
+    Assignment d = parse_solution("R_0_0_0 0.99999995\nS_0_1_0 1.00000002\n", m);
+    CHECK(d.at(var_r(0, 0, 0)) == 1.0 && d.at(var_s(0, 1, 0)) == 1.0);
+    CHECK_THROWS_CODE(parse_solution("R_0_0_0 0.5\n", m), Errc::NonIntegralBinary);
+    CHECK_THROWS_CODE(parse_solution("R_9_9_9 1\n", m), Errc::UnknownVariable);
+    CHECK(parse_solution("Status reading finished\nR_0_0_0 1\n", m).at(var_r(0, 0, 0)) == 1.0);
+    CHECK_THROWS_CODE(parse_solution("Infeasible - objective value 0\n", m), Errc::InfeasibleMarker);
+    CHECK_THROWS_CODE(parse_solution("# nothing here\n", m), Errc::EmptySolution);
+  });
+  run("format_solution round trips through parse_solution (fig2 exact)", [] {
+    Problem p = fixture("fig2");
+    MilpModel m = build_model(p);
+    Solution sol = solve_exact(p);
+    const std::string text = format_solution(sol.assignment);
+    Assignment back = parse_solution(text, m);
+    CHECK(back.objective_reported.has_value() && *back.objective_reported == sol.objective_ms);
+    bool same = true;
+    for (const auto& [ref, value] : sol.assignment.values) same = same && back.at(ref) == value;
+    for (const auto& [ref, value] : back.values) same = same && sol.assignment.at(ref) == value;
+    CHECK(same);
+    CHECK(format_solution(sol.assignment) == text);
+  });
   // ---- schedule.hpp: proj/tests/test_schedule.cpp:300-370
   run("replay accounts costs and memory (fig2 exact optimum)", [] {
     Problem p = fixture("fig2");
@@ -547,7 +583,20 @@ void device_cases() {
     CHECK(check_assignment(build_model(p), s.assignment).empty());
     CHECK(s.nodes_explored > 0);
   });
-  run("solve_search: F2 fig2 = 11.0 (LP bound 9.83: not proven)", [] {
+  run("solve_search: F2 fig2 = 11.0 (LP bound 9.83: not proven by the LP alone)", [] {
+    Problem p = fixture("fig2");
+    SearchParams sp;
+    sp.candidates_per_round = 1 << 15;
+    sp.rounds = 2;
+    sp.chain_iters = 20;
+    sp.exact_polish = false;
+    Solution s = solve_search(p, {}, sp);
+    CHECK(s.objective_ms == 11.0);
+    CHECK(s.status == SolveStatus::LimitReached);
+    CHECK(objective_value(s.assignment, p) == 11.0);
+    CHECK(check_assignment(build_model(p), s.assignment).empty());
+  });
+  run("solve_search + exact polish: fig2 proven optimal, the reference's twin (A on the gpu)", [] {
     Problem p = fixture("fig2");
     SearchParams sp;
     sp.candidates_per_round = 1 << 15;
@@ -555,9 +604,8 @@ void device_cases() {
     sp.chain_iters = 20;
     Solution s = solve_search(p, {}, sp);
     CHECK(s.objective_ms == 11.0);
-    CHECK(s.status == SolveStatus::LimitReached);
-    CHECK(objective_value(s.assignment, p) == 11.0);
-    CHECK(check_assignment(build_model(p), s.assignment).empty());
+    CHECK(s.status == SolveStatus::Optimal);
+    CHECK(s.assignment.at(var_r(1, 1, 1)) == 1.0);  // solve_exact's tail_less twin (test_solver.cpp:108-113)
   });
   run("solve_search: F1 at 3 MiB has no valid schedule", [] {
     Problem p = with_budgets(fixture("chain3"), {3 * kMiB});
