@@ -245,7 +245,8 @@ int eval_stream_device(const xe_problem* pr, const xe_model_opts& opts, const ui
       off = align16(off + bytes);
       return o;
     };
-    take(wide ? nch * 2048 * msz : 8 * NW * 256 * msz);  // mass tables at offset 0
+    const int nbl_bytes = (h.T - 64 * (NW - 1) + 7) / 8;  // row bytes of the last word
+    take(wide ? nch * 2048 * msz : (8 * (NW - 1) + (nbl_bytes <= 4 ? 4 : nbl_bytes <= 6 ? 6 : 8)) * 256 * msz);
     a.off_mass = take(msz * h.T);
     a.off_pmask = take(8 * h.T * NW);
     a.off_cons = take(8 * h.T * NW);
@@ -258,9 +259,10 @@ int eval_stream_device(const xe_problem* pr, const xe_model_opts& opts, const ui
     a.off_dst = take(4 * std::max(1, h.E));
     a.off_warp = off;
     // per warp: queue | fl[32] | cnt[32] | pk[32][maxd] | slow[32] | park[32]
-    const int park_bytes = 8 + 16 + 3 * 8 * maxd * NW + msz * maxd + 4;
+    const int pf_words = maxd * NW <= 4 ? maxd * NW : 1;  // Park::Rn / Sn
+    const int park_bytes = 8 + 16 + 8 * maxd * NW + 2 * 8 * pf_words + msz * maxd + 4;
     const int park_sz = (park_bytes + 7) & ~7;
-    a.warp_bytes = align16(static_cast<int>(sizeof(Job)) * kQCap + 4 * 32 + 4 * 32 + msz * 32 * maxd +
+    a.warp_bytes = align16(static_cast<int>(sizeof(Job)) * qcap(NW) + 4 * 32 + 4 * 32 + msz * 32 * maxd +
                            8 * 32 + 32 * park_sz + 64);
     a.smem_bytes = off + (wide ? kWideWarps : kWarps) * a.warp_bytes;
   };

@@ -50,6 +50,12 @@ namespace st {
 
 constexpr int kWarps = 8;
 constexpr int kQCap = 192;  // queue jobs per warp (one timestep adds <= 64)
+#ifndef XE_PREFETCH
+#define XE_PREFETCH 2
+#endif
+constexpr int kPrefetch = XE_PREFETCH;  // timesteps ahead (multi-word rows)
+// multi-word rows: a smaller queue keeps two CTAs per SM within shared memory
+__host__ __device__ constexpr int qcap(int nw) { return nw == 1 ? kQCap : 128; }
 constexpr int kKindA = 1;   // full general timestep
 constexpr int kKindB = 2;   // EQ11 / EQ16_HI rows of the timestep
 
@@ -263,9 +269,11 @@ __device__ __forceinline__ double run_job(const uint64_t* cwo, int t, int kind, 
 // job queue (the drain needs the registers; nothing is live across it).
 template <int MAXD, int NW, class M>
 struct Park {
+  // the prefetched rows of t+1 exist only when MAXD * NW <= 4 (PF)
+  static constexpr int PFD = MAXD * NW <= 4 ? MAXD : 1, PFW = MAXD * NW <= 4 ? NW : 1;
   double total;
   uint64_t fz, e12;
-  uint64_t Zp[MAXD][NW], Rn[MAXD][NW], Sn[MAXD][NW];
+  uint64_t Zp[MAXD][NW], Rn[PFD][PFW], Sn[PFD][PFW];
   M pk[MAXD];
   int nfast;
 };
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
   const DevProblem& P = a.P;
   const int D = cube::ndev<MAXD>(P), T = P.T, E = P.E;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int NBT = 8 * NW;  // byte tables (zero beyond the problem's bytes)
+  constexpr int NBT = 8 * (NW - 1) + NBL;  // byte tables of the row bytes that carry operators
   static_assert(TB == 8 || (TB == 11 && NW == 1), "11-bit mass tables cover one-word rows");
 
   M* s_mtab = reinterpret_cast<M*>(smem);  // [NBT][256] or [NBL][2048]
@@ -329,7 +337,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
     s_dst[i] = P.dst[i];
   }
   Job* queue = reinterpret_cast<Job*>(smem + a.off_warp + wid * a.warp_bytes);
-  uint32_t* s_fl = reinterpret_cast<uint32_t*>(queue + kQCap);
+  constexpr int QCAP = qcap(NW);
+  uint32_t* s_fl = reinterpret_cast<uint32_t*>(queue + QCAP);
   int32_t* s_cnt = reinterpret_cast<int32_t*>(s_fl + 32);
   M* s_pk = reinterpret_cast<M*>(s_cnt + 32);
   double* s_slow = reinterpret_cast<double*>(s_pk + 32 * MAXD);  // [32] deferred objective parts
@@ -423,6 +432,19 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
           }
         if (t + 1 < T) load_t(t + 1, Rn, Sn);
       } else {
+        // rows too wide to double-buffer in registers: prefetch the lines of
+        // t + kPrefetch into L2 (no registers) while t's are loaded
+        if (t + kPrefetch < T) {
+          const uint64_t* pn = cw + static_cast<int64_t>(t + kPrefetch) * NW * 32;
+#pragma unroll
+          for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+            for (int j = 0; j < NW; ++j)
+              if (d < D) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + d * dstride + j * 32));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + (D + d) * dstride + j * 32));
+              }
+        }
         load_t(t, R, S);
       }
       const int tw = NW == 1 ? 0 : (t >> 6), tb = t & 63;
@@ -511,7 +533,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
         const int q2 = q_cnt + __popc(bA);
         if (eq11) queue[q2 + __popc(bB & lt_mask)].meta = static_cast<uint32_t>(t - 1) | (lane << 10) | (kKindB << 15);
         q_cnt = q2 + __popc(bB);
-        if (q_cnt > kQCap - 64) {
+        if (q_cnt > QCAP - 64) {
           Park<MAXD, NW, M>& pp = park[lane];
           pp.total = total;
           pp.fz = fzS;
@@ -523,7 +545,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
               pp.Zp[d][j] = Zp[d][j];
-              if (PF) {
+              if constexpr (PF) {
                 pp.Rn[d][j] = Rn[d][j];
                 pp.Sn[d][j] = Sn[d][j];
               }
@@ -542,7 +564,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
               Zp[d][j] = pp.Zp[d][j];
-              if (PF) {
+              if constexpr (PF) {
                 Rn[d][j] = pp.Rn[d][j];
                 Sn[d][j] = pp.Sn[d][j];
               }
