@@ -142,7 +142,27 @@ __device__ __noinline__ M row_peak(Row<NW> Rd, Row<NW> Zd, Row<NW> Snd, Row<NW> 
 // Kind A returns the timestep's objective part (compute terms in (d,i)
 // order, then copy charges) and merges flags / EQ9 count / row peaks into the
 // owner's shared slots; kind B merges the EQ11 and EQ16_HI bits.
-template <int MAXD, int NW, class M>
+// Mass of the tensors of a bit row through the shared tables (the same
+// lookups as the streaming pass): TB = 8 byte tables, or TB = 11 chunks.
+template <int NW, class M, int NBL, int TB>
+__device__ __forceinline__ M table_mass(const Row<NW>& r, const M* mtab) {
+  M m = 0;
+  if (TB == 8) {
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const uint32_t lo = static_cast<uint32_t>(r.w[j]), hi = static_cast<uint32_t>(r.w[j] >> 32);
+#pragma unroll
+      for (int b = 0; b < (j == NW - 1 ? NBL : 8); ++b)
+        m += mtab[(8 * j + b) * 256 + (((b < 4 ? lo : hi) >> (8 * (b & 3))) & 0xffu)];
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NBL; ++c) m += mtab[c * 2048 + static_cast<int>((r.w[0] >> (11 * c)) & 0x7ffull)];
+  }
+  return m;
+}
+
+template <int MAXD, int NW, class M, int NBL, int TB>
 __device__ __forceinline__ double run_job(const uint64_t* cwo, int t, int kind, int owner, const StArgs* ap,
                                        const Sm<M> sm) {
   const StArgs& a = *ap;
@@ -252,7 +272,7 @@ __device__ __forceinline__ double run_job(const uint64_t* cwo, int t, int kind, 
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
     if (d >= D) continue;
-    const M base = mass_of<NW, M>(st.S[d], sm.mass);
+    const M base = table_mass<NW, M, NBL, TB>(st.S[d], sm.mtab);
     const int np = st.R[d].popc();
     M pkd = base;
     if (np >= 2)
@@ -388,7 +408,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
       for (int k = lane; k < q_cnt; k += 32) {
         const uint32_t m = queue[k].meta;
         const int owner = (m >> 10) & 31;
-        queue[k].part = run_job<MAXD, NW, M>(cw - lane + owner, static_cast<int>(m & 1023u), static_cast<int>(m >> 15),
+        queue[k].part = run_job<MAXD, NW, M, NBL, TB>(cw - lane + owner, static_cast<int>(m & 1023u), static_cast<int>(m >> 15),
                                              owner, &a, sm);
       }
       __syncwarp();
