@@ -22,6 +22,9 @@
 // One warp per candidate; the cube is assembled in shared memory and written
 // out with coalesced 16-byte stores.
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "bits.cuh"
 #include "xe_internal.hpp"
 
@@ -86,6 +89,155 @@ struct RoundArgs {
 
 constexpr int kRoundWarps = 4;
 
+// Steps 3-4 of one candidate (drop-and-recompute edits, perturbation): a
+// sequential walk over one cube; run by lane 0 of the candidate's warp
+// (round_kernel) or by one lane per candidate (round_batch_kernel) — the
+// same code, so both produce the same cubes.
+__device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* dev, const uint32_t* cons,
+                               const int* last, const int* elig, int n_elig_v, uint64_t c) {
+  const int D = a.D, T = a.T, W = a.W32;
+  (void)last;
+  auto consumer_at = [&](int u, int tt) {
+    uint32_t hit = 0u;
+    for (int w = 0; w < W; ++w) {
+      uint32_t r = 0u;
+      for (int d = 0; d < D; ++d) r |= cube[(d * T + tt) * W + w];
+      hit |= r & cons[u * W + w];
+    }
+    return hit != 0u;
+  };
+  auto bset = [&](int which, int d, int t, int i) {
+    cube[((which * D + d) * T + t) * W + (i >> 5)] |= 1u << (i & 31);
+  };
+  auto bclr = [&](int which, int d, int t, int i) {
+    cube[((which * D + d) * T + t) * W + (i >> 5)] &= ~(1u << (i & 31));
+  };
+  auto bit_get = [&](int which, int d, int t, int i) -> bool {
+    return (cube[((which * D + d) * T + t) * W + (i >> 5)] >> (i & 31)) & 1u;
+  };
+  Philox rng(a.seed, c, 0x1u);
+  for (int ed = 0; ed < a.edits; ++ed) {
+    if (rng.uniform() >= 0.6) continue;
+    int i = 0, t = -1, lp_dev = -1;
+    if (a.n_rc > 0 && rng.uniform() < 0.7) {
+      // where the LP relaxation recomputes: (d, t, i) drawn with weight x(R(d,t,i))
+      const double u = rng.uniform() * a.rc_cdf[a.n_rc - 1];
+      int lo = 0, hi = a.n_rc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a.rc_cdf[mid] > u) hi = mid;
+        else lo = mid + 1;
+      }
+      const int code = a.rc_code[lo];
+      i = code % T;
+      t = code / T % T;
+      lp_dev = code / (T * T);
+    } else {
+      // op i with a consumer beyond i+1, chosen uniformly among eligible ops
+      const int n_el = n_elig_v;
+      if (n_el == 0) break;
+      i = elig[rng.below(n_el)];
+      // consumer t > i+1 of i, uniformly among its consumers (ascending)
+      int n_c = 0;
+      for (int w = 0; w < W; ++w) {
+        const int lo = w * 32;
+        uint32_t m = cons[i * W + w];
+        if (lo + 32 <= i + 2) m = 0u;
+        else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
+        n_c += __popc(m);
+      }
+      int pc = rng.below(n_c);
+      for (int w = 0; w < W && t < 0; ++w) {
+        const int lo = w * 32;
+        uint32_t m = cons[i * W + w];
+        if (lo + 32 <= i + 2) m = 0u;
+        else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
+        const int pcnt = __popc(m);
+        if (pc < pcnt) {
+          for (int q = 0; q < pc; ++q) m &= m - 1;
+          t = lo + __ffs(m) - 1;
+        }
+        pc -= pcnt;
+      }
+    }
+    // the drop window must not cover a timestep where i is needed: any
+    // earlier computation (diagonal or recomputed) of a consumer of i
+    int a0 = i + 1;
+    for (int tt = t - 1; tt > i; --tt)
+      if (consumer_at(i, tt)) {
+        a0 = tt + 1;
+        break;
+      }
+    if (a0 > t) continue;
+    // drop the whole window when the LP chose the spot, else a random tail of it
+    const int a1 = lp_dev >= 0 ? a0 : a0 + rng.below(t - a0 + 1);
+    int dn = lp_dev >= 0 ? lp_dev : (rng.uniform() < 0.5 ? rng.below(D) : dev[t]);
+    if (a.cost[dn * T + i] >= 1.0e9) dn = dev[i];
+    // recompute op v at t on device dr, dropping its saves on dev-of-v
+    // over [from, t]; later saves follow it to dr (EQ11 needs a holder at t)
+    auto recompute_at = [&](int v, int from, int dr) {
+      const int dv = dev[v];
+      for (int tt = from; tt <= t; ++tt) bclr(1, dv, tt, v);
+      bset(0, dr, t, v);
+      if (dr != dv)
+        for (int tt = t + 1; tt < T; ++tt)
+          if (bit_get(1, dv, tt, v)) {
+            bclr(1, dv, tt, v);
+            bset(1, dr, tt, v);
+          }
+    };
+    recompute_at(i, a1, dn);
+    // parents of every op recomputed at t: keep them saved until t, or
+    // (probability 1/2) recompute them at t too, dropping their own save
+    // windows — chains of recomputation.  A recomputed parent runs on its
+    // child's device or (probability 1/4) another one: a chain may cross
+    // devices within the timestep, so a memory-tight device need not hold
+    // the chain's intermediate tensors (config 2's optimum recomputes
+    // ops 0-1 on the cpu and 2-3 on the gpu at t = 39)
+    int stack[32], sdev[32], sp = 0;
+    stack[sp] = i;
+    sdev[sp++] = dn;
+    while (sp > 0) {
+      --sp;
+      const int v = stack[sp], dvn = sdev[sp];
+      for (int k2 = a.in_ptr[v]; k2 < a.in_ptr[v + 1]; ++k2) {
+        const int p = a.src[a.in_edge[k2]];
+        bool avail = false;
+        for (int d = 0; d < D; ++d) avail |= bit_get(0, d, t, p) || bit_get(1, d, t, p);
+        if (avail) continue;
+        int dr = dvn;
+        if (D > 1 && rng.uniform() < 0.25) dr = (dvn + 1 + rng.below(D - 1)) % D;
+        if (a.cost[dr * T + p] >= 1.0e9) dr = dvn;
+        if (sp < 32 && a.cost[dr * T + p] < 1.0e9 && rng.uniform() < 0.5) {
+          // first step after p's last use before t
+          int from = p + 1;
+          for (int tt = t - 1; tt > p; --tt)
+            if (consumer_at(p, tt)) {
+              from = tt + 1;
+              break;
+            }
+          recompute_at(p, from, dr);
+          stack[sp] = p;
+          sdev[sp++] = dr;
+          continue;
+        }
+        const int dp = dev[p];
+        int ls = p;
+        for (int tt = p + 1; tt <= t; ++tt)
+          if (bit_get(1, dp, tt, p)) ls = tt;
+        for (int tt = ls + 1; tt <= t; ++tt) bset(1, dp, tt, p);
+      }
+    }
+  }
+  // 4. perturbation
+  if (rng.uniform() < a.perturb) {
+    const int which = rng.below(2), d = rng.below(D), t = rng.below(T), i = rng.below(T);
+    cube[((which * D + d) * T + t) * W + (i >> 5)] ^= 1u << (i & 31);
+  }
+
+}
+
+
 __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -113,16 +265,6 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
     *n_elig = ne;
   }
   __syncthreads();
-  // some consumer of u computed at step tt (any device)
-  auto consumer_at = [&](int u, int tt) {
-    uint32_t hit = 0u;
-    for (int w = 0; w < W; ++w) {
-      uint32_t r = 0u;
-      for (int d = 0; d < D; ++d) r |= cube[(d * T + tt) * W + w];
-      hit |= r & cons[u * W + w];
-    }
-    return hit != 0u;
-  };
   auto bit_set = [&](int which, int d, int t, int i) {
     atomicOr(&cube[((which * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
   };
@@ -206,131 +348,104 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       for (int t = i + 1; t <= last[i]; ++t) bit_set(1, dev[i], t, i);
     }
     __syncwarp();
-    // 3. drop-and-recompute edits (lane 0, sequential, O(T + E) each)
-    if (lane == 0) {
-      Philox rng(a.seed, c, 0x1u);
-      for (int ed = 0; ed < a.edits; ++ed) {
-        if (rng.uniform() >= 0.6) continue;
-        int i = 0, t = -1, lp_dev = -1;
-        if (a.n_rc > 0 && rng.uniform() < 0.7) {
-          // where the LP relaxation recomputes: (d, t, i) drawn with weight x(R(d,t,i))
-          const double u = rng.uniform() * a.rc_cdf[a.n_rc - 1];
-          int lo = 0, hi = a.n_rc - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (a.rc_cdf[mid] > u) hi = mid;
-            else lo = mid + 1;
-          }
-          const int code = a.rc_code[lo];
-          i = code % T;
-          t = code / T % T;
-          lp_dev = code / (T * T);
-        } else {
-          // op i with a consumer beyond i+1, chosen uniformly among eligible ops
-          const int n_el = *n_elig;
-          if (n_el == 0) break;
-          i = elig[rng.below(n_el)];
-          // consumer t > i+1 of i, uniformly among its consumers (ascending)
-          int n_c = 0;
-          for (int w = 0; w < W; ++w) {
-            const int lo = w * 32;
-            uint32_t m = cons[i * W + w];
-            if (lo + 32 <= i + 2) m = 0u;
-            else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
-            n_c += __popc(m);
-          }
-          int pc = rng.below(n_c);
-          for (int w = 0; w < W && t < 0; ++w) {
-            const int lo = w * 32;
-            uint32_t m = cons[i * W + w];
-            if (lo + 32 <= i + 2) m = 0u;
-            else if (lo <= i + 1) m &= ~0u << (i + 2 - lo);
-            const int pcnt = __popc(m);
-            if (pc < pcnt) {
-              for (int q = 0; q < pc; ++q) m &= m - 1;
-              t = lo + __ffs(m) - 1;
-            }
-            pc -= pcnt;
-          }
-        }
-        // the drop window must not cover a timestep where i is needed: any
-        // earlier computation (diagonal or recomputed) of a consumer of i
-        int a0 = i + 1;
-        for (int tt = t - 1; tt > i; --tt)
-          if (consumer_at(i, tt)) {
-            a0 = tt + 1;
-            break;
-          }
-        if (a0 > t) continue;
-        // drop the whole window when the LP chose the spot, else a random tail of it
-        const int a1 = lp_dev >= 0 ? a0 : a0 + rng.below(t - a0 + 1);
-        int dn = lp_dev >= 0 ? lp_dev : (rng.uniform() < 0.5 ? rng.below(D) : dev[t]);
-        if (a.cost[dn * T + i] >= 1.0e9) dn = dev[i];
-        // recompute op v at t on device dr, dropping its saves on dev-of-v
-        // over [from, t]; later saves follow it to dr (EQ11 needs a holder at t)
-        auto recompute_at = [&](int v, int from, int dr) {
-          const int dv = dev[v];
-          for (int tt = from; tt <= t; ++tt) bclr(1, dv, tt, v);
-          bset(0, dr, t, v);
-          if (dr != dv)
-            for (int tt = t + 1; tt < T; ++tt)
-              if (bit_get(1, dv, tt, v)) {
-                bclr(1, dv, tt, v);
-                bset(1, dr, tt, v);
-              }
-        };
-        recompute_at(i, a1, dn);
-        // parents of every op recomputed at t: keep them saved until t, or
-        // (probability 1/2) recompute them at t too, dropping their own save
-        // windows — chains of recomputation.  A recomputed parent runs on its
-        // child's device or (probability 1/4) another one: a chain may cross
-        // devices within the timestep, so a memory-tight device need not hold
-        // the chain's intermediate tensors (config 2's optimum recomputes
-        // ops 0-1 on the cpu and 2-3 on the gpu at t = 39)
-        int stack[32], sdev[32], sp = 0;
-        stack[sp] = i;
-        sdev[sp++] = dn;
-        while (sp > 0) {
-          --sp;
-          const int v = stack[sp], dvn = sdev[sp];
-          for (int k2 = a.in_ptr[v]; k2 < a.in_ptr[v + 1]; ++k2) {
-            const int p = a.src[a.in_edge[k2]];
-            bool avail = false;
-            for (int d = 0; d < D; ++d) avail |= bit_get(0, d, t, p) || bit_get(1, d, t, p);
-            if (avail) continue;
-            int dr = dvn;
-            if (D > 1 && rng.uniform() < 0.25) dr = (dvn + 1 + rng.below(D - 1)) % D;
-            if (a.cost[dr * T + p] >= 1.0e9) dr = dvn;
-            if (sp < 32 && a.cost[dr * T + p] < 1.0e9 && rng.uniform() < 0.5) {
-              // first step after p's last use before t
-              int from = p + 1;
-              for (int tt = t - 1; tt > p; --tt)
-                if (consumer_at(p, tt)) {
-                  from = tt + 1;
-                  break;
-                }
-              recompute_at(p, from, dr);
-              stack[sp] = p;
-              sdev[sp++] = dr;
-              continue;
-            }
-            const int dp = dev[p];
-            int ls = p;
-            for (int tt = p + 1; tt <= t; ++tt)
-              if (bit_get(1, dp, tt, p)) ls = tt;
-            for (int tt = ls + 1; tt <= t; ++tt) bset(1, dp, tt, p);
-          }
-        }
-      }
-      // 4. perturbation
-      if (rng.uniform() < a.perturb) {
-        const int which = rng.below(2), d = rng.below(D), t = rng.below(T), i = rng.below(T);
-        cube[((which * D + d) * T + t) * W + (i >> 5)] ^= 1u << (i & 31);
-      }
-    }
+    // 3-4. drop-and-recompute edits and perturbation (lane 0, sequential)
+    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c);
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k) * words;
     for (int i = lane; i < words; i += 32) out[i] = cube[i];
+    __syncwarp();
+  }
+}
+
+// The rounding path (no base cube) with one lane per candidate for the
+// sequential part: a warp builds 32 candidates' placements and minimal saves
+// (lanes over operators, one candidate after another), then every lane runs
+// steps 3-4 on its own candidate's cube, then the 32 cubes leave with
+// coalesced stores.  Same Philox streams and the same edit code as
+// round_kernel, so the same cubes; used when 32 cubes per warp fit in shared
+// memory.
+__global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int warps, int B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int D = a.D, T = a.T, W = a.W32;
+  const int words = 2 * D * T * W, stride = words + T;  // per candidate: cube, then dev
+  uint32_t* cons = reinterpret_cast<uint32_t*>(smem);
+  int* last = reinterpret_cast<int*>(cons + T * W);
+  int* elig = last + T;
+  int* n_elig = elig + T;
+  uint32_t* wbuf = reinterpret_cast<uint32_t*>(n_elig + 1) + static_cast<size_t>(wid) * B * stride;
+  for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) {
+    atomicOr(&cons[a.src[e] * W + (a.dst[e] >> 5)], 1u << (a.dst[e] & 31));
+    atomicMax(&last[a.src[e]], a.dst[e]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ne = 0;
+    for (int j = 0; j < T; ++j)
+      if (last[j] > j + 1) elig[ne++] = j;
+    *n_elig = ne;
+  }
+  __syncthreads();
+  const int n_el = *n_elig;
+  for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * warps + wid) * B; k0 < a.n;
+       k0 += static_cast<int64_t>(gridDim.x) * warps * B) {
+    const int nb = static_cast<int>(a.n - k0 < B ? a.n - k0 : B);
+    for (int j = 0; j < nb; ++j) {
+      const uint64_t c = static_cast<uint64_t>(a.first + k0 + j);
+      uint32_t* cube = wbuf + static_cast<size_t>(j) * stride;
+      int* dev = reinterpret_cast<int*>(cube + words);
+      for (int i = lane; i < words; i += 32) cube[i] = 0u;
+      // 1. placement, one Philox stream per (candidate, op)
+      for (int i = lane; i < T; i += 32) {
+        Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
+        double tot = 0.0;
+        for (int d = 0; d < D; ++d) {
+          if (a.cost[d * T + i] >= 1.0e9) continue;
+          tot += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
+        }
+        int pick = 0;
+        if (tot == 0.0) {
+          double best = 1e300;
+          for (int d = 0; d < D; ++d)
+            if (a.cost[d * T + i] < best) best = a.cost[d * T + i], pick = d;
+        } else {
+          double u = rng.uniform() * tot, acc = 0.0;
+          int lastok = 0;
+          pick = -1;
+          for (int d = 0; d < D; ++d) {
+            if (a.cost[d * T + i] >= 1.0e9) continue;
+            acc += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
+            lastok = d;
+            if (pick < 0 && u < acc) pick = d;
+          }
+          if (pick < 0) pick = lastok;
+        }
+        dev[i] = pick;
+      }
+      __syncwarp();
+      // 2. diagonal + minimal-save
+      for (int i = lane; i < T; i += 32) {
+        const int d = dev[i];
+        atomicOr(&cube[((0 * D + d) * T + i) * W + (i >> 5)], 1u << (i & 31));
+        for (int t = i + 1; t <= last[i]; ++t) atomicOr(&cube[((1 * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
+      }
+      __syncwarp();
+    }
+    // 3-4. one lane per candidate
+    if (lane < nb) {
+      uint32_t* cube = wbuf + static_cast<size_t>(lane) * stride;
+      edit_candidate(a, cube, reinterpret_cast<const int*>(cube + words), cons, last, elig, n_el,
+                     static_cast<uint64_t>(a.first + k0 + lane));
+    }
+    __syncwarp();
+    uint32_t* out = a.out + static_cast<size_t>(k0) * words;
+    for (int j = 0; j < nb; ++j) {
+      const uint32_t* cube = wbuf + static_cast<size_t>(j) * stride;
+      for (int i = lane; i < words; i += 32) out[static_cast<size_t>(j) * words + i] = cube[i];
+    }
     __syncwarp();
   }
 }
@@ -691,6 +806,29 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   const int smem = (h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T)) * 4;
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
+  {  // lane per candidate when 32 cubes per warp fit (base cubes keep round_kernel)
+    const int tables = (h.T * a.W32 + 2 * h.T + 1) * 4;
+    const char* e = std::getenv("XE_ROUND_BATCH");
+    const int B = e ? std::max(0, std::min(32, std::atoi(e))) : 8;  // candidates per warp (0: round_kernel); 8 measured best
+    const int per_warp = B * (words + h.T) * 4;
+    const int warps = B > 0 ? std::min(8, (limit - tables) / std::max(1, per_warp)) : 0;
+    if (!base && warps >= 1) {
+      const int bsmem = tables + warps * per_warp;
+      XE_CUDA(cudaFuncSetAttribute(round_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
+      int nsm = 0;
+      XE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, pr->device));
+      int per_sm = 0;
+      XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, round_batch_kernel, warps * 32, bsmem));
+      const int64_t want = (n + static_cast<int64_t>(B) * warps - 1) / (static_cast<int64_t>(B) * warps);
+      const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(nsm) * std::max(1, per_sm))));
+      if (n > 0) {
+        round_batch_kernel<<<grid, warps * 32, bsmem, s>>>(a, warps, B);
+        XE_CUDA(cudaGetLastError());
+      }
+      if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+  }
   if (smem > limit) fail(XE_ERR_TOO_LARGE, "candidate cube too large for the rounding kernel");
   XE_CUDA(cudaFuncSetAttribute(round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nsm = 0;

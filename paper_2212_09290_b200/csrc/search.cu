@@ -298,9 +298,15 @@ void search_device(const xe_problem* pr, const xe_model_opts& mo, const xe_searc
     nobj.alloc(PM);
     nflags.alloc(PM);
     npeak.alloc(static_cast<size_t>(PM) * h.D);
-    double gbest = *std::min_element(cur_h.begin(), cur_h.end());
+    const auto mi0 = std::min_element(cur_h.begin(), cur_h.end());
+    double gbest = *mi0;
     DevBuf<uint32_t> gcube;
     gcube.alloc(words);
+    // the population's best chain is the local search's incumbent until a
+    // chain improves on it (its score may sit an ulp below the exact
+    // rounding objective: the streaming evaluator's reassociation)
+    XE_CUDA(cudaMemcpyAsync(gcube.p, bases.p + static_cast<size_t>(mi0 - cur_h.begin()) * words, words * 4,
+                            cudaMemcpyDeviceToDevice, s));
     const uint64_t ls_seed = (so.seed * 1000003ull + static_cast<uint64_t>(so.rank)) & 0xFFFFFFFFFFFFull;
     for (int it = 0; it < so.chain_iters; ++it) {
       if (out_of_time()) {

@@ -170,3 +170,19 @@ def test_move_placements_neighbours():
     allowed = cost.T < 1e9  # [T, D]
     assert allowed[np.arange(prob.T)[None, :], h].all()
     assert (h[:, 0] == 0).all()
+
+
+@pytest.mark.parametrize("name", ["fig2", "vgg16"])
+def test_batched_rounding_equals_warp_rounding(name):
+    # round_batch_kernel (one lane per candidate for the edits) and round_kernel
+    # (lane 0 per candidate) run the same Philox streams and edit code
+    import os
+    text = golden_problem_text(name) if name == "fig2" else configs.CONFIGS[name]()
+    prob = xe.Problem.from_json(text)
+    a = xe.round_cubes(prob, 3000, seed=13, first=77, edits=4, perturb=0.2)
+    os.environ["XE_ROUND_BATCH"] = "0"  # the warp-per-candidate kernel
+    try:
+        b = xe.round_cubes(prob, 3000, seed=13, first=77, edits=4, perturb=0.2)
+    finally:
+        del os.environ["XE_ROUND_BATCH"]
+    assert torch.equal(a, b)
