@@ -249,6 +249,10 @@ typedef struct xe_best {
  * NULL members to skip writing them.  best (host, may be NULL) receives the
  * argmin over candidates whose flags & valid_mask == 0.  stream: a cudaStream_t;
  * NULL is the legacy default stream (as in every CUDA library). */
+/* A problem handle owns the staging and scratch buffers of these calls: use a
+ * handle from one host thread and on one stream at a time (calls on different
+ * streams must be ordered by the caller); open one handle per stream
+ * otherwise. */
 int xe_eval_cubes(const xe_problem* p, const xe_model_opts* opts, const uint32_t* cubes,
                   int64_t n, xe_eval_out* out, uint32_t valid_mask, xe_best* best,
                   void* stream);

@@ -54,6 +54,10 @@ constexpr int kQCap = 192;  // queue jobs per warp (one timestep adds <= 64)
 #define XE_PREFETCH 2
 #endif
 constexpr int kPrefetch = XE_PREFETCH;  // timesteps ahead (multi-word rows)
+#ifndef XE_T_UNROLL
+#define XE_T_UNROLL 1
+#endif
+constexpr int kTUnroll = XE_T_UNROLL;  // unroll of the streaming pass over t
 // multi-word rows: a smaller queue keeps two CTAs per SM within shared memory
 __host__ __device__ constexpr int qcap(int nw) { return nw == 1 ? kQCap : 128; }
 constexpr int kKindA = 1;   // full general timestep
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
     };
     if (PF) load_t(0, Rn, Sn);
 
-#pragma unroll 1
+#pragma unroll kTUnroll
     for (int t = 0; t < T; ++t) {
       uint64_t R[MAXD][NW], S[MAXD][NW];
       if (PF) {
