@@ -209,12 +209,12 @@ __global__ void sell_size_kernel(const int32_t* slen, int64_t len, int64_t nlong
   GRID_LOOP(k, nlong + ns + 2) {
     int64_t v = 0;
     if (k < nlong) {
-      v = slen[k];
+      v = (slen[k] + 1) & ~1;  // even: every slice starts 16-byte aligned
     } else if (k > nlong && k <= nlong + ns) {
       const int64_t r0 = nlong + (k - nlong - 1) * 32;
       int32_t w = 0;
       for (int64_t r = r0; r < r0 + 32 && r < len; ++r) w = max(w, slen[r]);
-      v = 32 * static_cast<int64_t>(w);
+      v = 32 * static_cast<int64_t>((w + 1) & ~1);  // an even width: entries go in lane pairs
     }
     sz[k] = v;
   }
@@ -230,6 +230,10 @@ __global__ void sell_fill_kernel(const int64_t* p, const int32_t* idx_in, const 
         idx[o + t] = remap[idx_in[q0 + t]];
         v[o + t] = v_in[q0 + t];
       }
+      if (l & 1) {  // the even padding entry: 0 * x[0]
+        idx[o + l] = 0;
+        v[o + l] = 0.0;
+      }
       continue;
     }
     const int64_t r = k - nlong, sl = r >> 5, row = k;
@@ -241,10 +245,14 @@ __global__ void sell_fill_kernel(const int64_t* p, const int32_t* idx_in, const 
       q0 = p[i];
       l = p[i + 1] - q0;
     }
+    // entry t of this lane at base + 64 (t / 2) + 2 lane + t % 2: a lane's
+    // consecutive entries are adjacent, so one 8-byte index load and one
+    // 16-byte value load fetch two entries
     for (int64_t t = 0; t < w; ++t) {
       const bool in = t < l;
-      idx[base + t * 32 + lane] = in ? remap[idx_in[q0 + t]] : 0;
-      v[base + t * 32 + lane] = in ? v_in[q0 + t] : 0.0;
+      const int64_t at = base + 64 * (t >> 1) + 2 * lane + (t & 1);
+      idx[at] = in ? remap[idx_in[q0 + t]] : 0;
+      v[at] = in ? v_in[q0 + t] : 0.0;
     }
   }
 }
@@ -328,12 +336,17 @@ __device__ __forceinline__ double long_dot(const SellView& A, int64_t w, const d
 // dot product of this lane's row of slice sl with x
 __device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const double* __restrict__ x, int lane) {
   const int64_t base = A.ptr[A.nlong + 1 + sl];
-  const int w = static_cast<int>((A.ptr[A.nlong + 2 + sl] - base) >> 5);
-  const int32_t* ip = A.idx + base + lane;
-  const double* vp = A.v + base + lane;
+  const int w2 = static_cast<int>((A.ptr[A.nlong + 2 + sl] - base) >> 6);  // entry pairs
+  const int2* ip = reinterpret_cast<const int2*>(A.idx + base) + lane;
+  const double2* vp = reinterpret_cast<const double2*>(A.v + base) + lane;
   double acc = 0.0;
-#pragma unroll 4
-  for (int t = 0; t < w; ++t) acc += __ldg(vp + 32 * t) * __ldg(x + __ldg(ip + 32 * t));
+#pragma unroll 2
+  for (int t = 0; t < w2; ++t) {
+    const int2 ix = __ldg(ip + 32 * t);
+    const double2 vv = __ldg(vp + 32 * t);
+    acc += vv.x * __ldg(x + ix.x);
+    acc += vv.y * __ldg(x + ix.y);
+  }
   return acc;
 }
 
