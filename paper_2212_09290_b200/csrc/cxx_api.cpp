@@ -773,19 +773,7 @@ BatchResult evaluate_candidates(const Problem& p, const ModelOptions& opts,
 
 // ============================ mps_io.hpp ===================================
 
-std::string format_number(double v) {
-  char buf[64];
-  if (v == 0.0) return "0";
-  if (std::isfinite(v) && v == std::floor(v) && std::fabs(v) < 1e15) {
-    std::snprintf(buf, sizeof buf, "%.0f", v);
-    return buf;
-  }
-  for (int prec = 1; prec <= 17; ++prec) {
-    std::snprintf(buf, sizeof buf, "%.*g", prec, v);
-    if (std::strtod(buf, nullptr) == v) break;
-  }
-  return buf;
-}
+std::string format_number(double v) { return xe::format_number(v); }
 
 std::string var_name(const VarRef& v) {
   static const char fam[] = "RSZFUP";

@@ -21,12 +21,9 @@
 #include "csr.hpp"
 
 namespace xe {
-namespace {
 
-const char* const kTag[14] = {"EQ7",     "EQ8",     "EQ9",     "EQ10",   "EQ11",       "EQ12",        "EQ13",
-                              "EQ14",    "EQ16_LO", "EQ16_HI", "Z_LINK", "P_LINK", "ENERGY_DEV", "ENERGY_TOTAL"};
-constexpr uint8_t kPLink = 11;
-
+// format_number (mps_io.cpp:14-27): the library's one copy (the C++ API's
+// xengine::format_number forwards here)
 std::string format_number(double v) {
   char buf[64];
   if (v == 0.0) return "0";
@@ -40,6 +37,12 @@ std::string format_number(double v) {
   }
   return buf;
 }
+
+namespace {
+
+const char* const kTag[14] = {"EQ7",     "EQ8",     "EQ9",     "EQ10",   "EQ11",       "EQ12",        "EQ13",
+                              "EQ14",    "EQ16_LO", "EQ16_HI", "Z_LINK", "P_LINK", "ENERGY_DEV", "ENERGY_TOTAL"};
+constexpr uint8_t kPLink = 11;
 
 struct Out {
   std::string s;

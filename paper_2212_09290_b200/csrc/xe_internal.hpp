@@ -125,6 +125,7 @@ struct ParsedDoc {
   std::vector<std::map<std::pair<int, int>, double>> overrides;  // per edge
 };
 ParsedDoc parse_problem_document(const std::string& text);  // loader.cpp
+std::string format_number(double v);                        // mps_writer.cpp (mps_io.cpp:14-27)
 
 // Forward network -> training graph (make_training_graph, problem.cpp:280-338,
 // generalised from a layer chain to a forward DAG): op 0 = the input
