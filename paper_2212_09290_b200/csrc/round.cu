@@ -812,7 +812,9 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     const int B = e ? std::max(0, std::min(32, std::atoi(e))) : 8;  // candidates per warp (0: round_kernel); 8 measured best
     const int per_warp = B * (words + h.T) * 4;
     const int warps = B > 0 ? std::min(8, (limit - tables) / std::max(1, per_warp)) : 0;
-    if (!base && warps >= 1) {
+    // below 4 warps per CTA (large cubes: ResNet-50 holds one) the warp per
+    // candidate kernel keeps more candidates in flight
+    if (!base && warps >= 4) {
       const int bsmem = tables + warps * per_warp;
       XE_CUDA(cudaFuncSetAttribute(round_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bsmem));
       int nsm = 0;
