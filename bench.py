@@ -150,6 +150,7 @@ def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
     import paper_2212_09290_b200 as xe
     prob = xe.Problem.from_json(doc_fn())
     k1_wall, model = _timed(lambda: xe.build_model(prob), warmup=1, reps=1)
+    mps_wall, mps_len = _timed(lambda: len(model.write_mps()), warmup=1, reps=3)
     lp = xe.pdhg_solve(model, tol=1e-7, max_iters=1000000, return_x=True)
     it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
     x = torch.from_numpy(lp.x).cuda()
@@ -166,6 +167,8 @@ def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
          "k1_build": {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "device_ms": model.build_ms(),
                       "wall_ms": 1e3 * k1_wall,
                       "achieved_gbs": (12 * model.nnz + 8 * (model.n_rows + 1) + 26 * model.n_cols) / (model.build_ms() / 1e3) / 1e9},
+         "write_mps": {"bytes": mps_len, "wall_ms": 1e3 * mps_wall,
+                       "path": "device text emission (mps_device.cu) + download into the returned bytes"},
          "pdhg": {"metric": "PDHG iters/sec", "iters": lp.iters, "converged": lp.converged, "certified": lp.certified,
                   "iters_per_s": lp.iters / (lp.solve_ms / 1e3), "time_to_tol_ms": lp.solve_ms, "tol": 1e-7,
                   "objective": lp.primal_obj, "dual_bound": lp.dual_obj,

@@ -25,6 +25,10 @@ import numpy as np
 from . import _lib
 from ._lib import LIB, check
 
+_new_bytes = C.pythonapi.PyBytes_FromStringAndSize
+_new_bytes.restype = C.py_object
+_new_bytes.argtypes = [C.c_void_p, C.c_ssize_t]
+
 
 @dataclass
 class ModelOptions:
@@ -437,9 +441,11 @@ class Model:
         """write_mps (mps_io.cpp:109-199), byte-identical."""
         n = C.c_size_t()
         check(LIB.xe_write_mps(self._h, None, C.byref(n)))
-        buf = C.create_string_buffer(n.value)
-        check(LIB.xe_write_mps(self._h, buf, C.byref(n)))
-        return buf.raw[: n.value]
+        # the text is downloaded straight into a fresh, not yet shared bytes
+        # object (one host pass instead of buffer + copy)
+        out = _new_bytes(None, n.value)
+        check(LIB.xe_write_mps(self._h, C.c_char_p(out), C.byref(n)))
+        return out
 
 
 @dataclass

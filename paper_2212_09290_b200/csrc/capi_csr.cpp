@@ -1,7 +1,10 @@
 // SPDX-License-Identifier: Apache-2.0
 // C ABI for K1 (model assembly) — include/xengine_b200.h.
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+
+#include <sys/mman.h>
 
 #include "csr.hpp"
 
@@ -13,8 +16,40 @@ std::vector<T> down(const T* p, size_t n, cudaStream_t s) {
   if (n) XE_CUDA(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
   return v;
 }
+constexpr uintptr_t kHuge = uintptr_t(2) << 20;
 }  // namespace
 int64_t check_rows_host(xe_csr* m, const double* x_host, double tol, double* viol_host);  // complete.cu
+
+// the host writer (mps_writer.cpp): QUADOBJ models, XE_MPS_HOST=1
+void mps_host(xe_csr* m) {
+  build_csc(m, m->stream);
+  cudaStream_t s = m->stream;
+  const xe_csr_info& in = m->info;
+  CsrHost h;
+  h.D = in.D;
+  h.T = in.T;
+  h.E = in.E;
+  h.n_rows = in.n_rows;
+  h.nnz = in.nnz;
+  h.n_cols = in.n_cols;
+  h.quad = m->opts.quadratic_objective != 0;
+  h.col_ptr = down(m->col_ptr.p, static_cast<size_t>(in.n_cols) + 1, s);
+  h.crow = down(m->crow.p, static_cast<size_t>(in.nnz), s);
+  h.cval = down(m->cval.p, static_cast<size_t>(in.nnz), s);
+  h.ordinal = down(m->ordinal.p, static_cast<size_t>(in.n_rows), s);
+  h.rhs = down(m->rhs.p, static_cast<size_t>(in.n_rows), s);
+  h.sense = down(m->sense.p, static_cast<size_t>(in.n_rows), s);
+  h.tag = down(m->tag.p, static_cast<size_t>(in.n_rows), s);
+  h.obj = down(m->obj.p, static_cast<size_t>(in.n_cols), s);
+  h.present = down(m->present.p, static_cast<size_t>(in.n_cols), s);
+  h.ub = down(m->ub.p, static_cast<size_t>(in.n_cols), s);
+  h.kind = down(m->kind.p, static_cast<size_t>(in.n_cols), s);
+  XE_CUDA(cudaStreamSynchronize(s));
+  h.w = m->prob->h.w;
+  h.src = m->prob->h.src;
+  h.dst = m->prob->h.dst;
+  m->mps = mps_text(h);
+}
 }  // namespace xe
 
 using namespace xe;
@@ -179,44 +214,37 @@ int xe_check_rows(xe_csr* m, const double* x, double tol, double* viol, int64_t*
 int xe_write_mps(xe_csr* m, char* buf, size_t* len) {
   return guard([&] {
     if (!m || !len) fail(XE_ERR_ARG, "null argument");
-    if (!buf || m->mps.empty()) {
+    if (!buf || (m->mps.empty() && !m->mps_dev.p)) {
       require_uploaded(m->prob);
-      build_csc(m, m->stream);
-      cudaStream_t s = m->stream;
-      const xe_csr_info& in = m->info;
-      CsrHost h;
-      h.D = in.D;
-      h.T = in.T;
-      h.E = in.E;
-      h.n_rows = in.n_rows;
-      h.nnz = in.nnz;
-      h.n_cols = in.n_cols;
-      h.quad = m->opts.quadratic_objective != 0;
-      h.col_ptr = down(m->col_ptr.p, static_cast<size_t>(in.n_cols) + 1, s);
-      h.crow = down(m->crow.p, static_cast<size_t>(in.nnz), s);
-      h.cval = down(m->cval.p, static_cast<size_t>(in.nnz), s);
-      h.ordinal = down(m->ordinal.p, static_cast<size_t>(in.n_rows), s);
-      h.rhs = down(m->rhs.p, static_cast<size_t>(in.n_rows), s);
-      h.sense = down(m->sense.p, static_cast<size_t>(in.n_rows), s);
-      h.tag = down(m->tag.p, static_cast<size_t>(in.n_rows), s);
-      h.obj = down(m->obj.p, static_cast<size_t>(in.n_cols), s);
-      h.present = down(m->present.p, static_cast<size_t>(in.n_cols), s);
-      h.ub = down(m->ub.p, static_cast<size_t>(in.n_cols), s);
-      h.kind = down(m->kind.p, static_cast<size_t>(in.n_cols), s);
-      XE_CUDA(cudaStreamSynchronize(s));
-      h.w = m->prob->h.w;
-      h.src = m->prob->h.src;
-      h.dst = m->prob->h.dst;
-      m->mps = mps_text(h);
+      std::string().swap(m->mps);
+      m->mps_dev.release();
+      const char* e = std::getenv("XE_MPS_HOST");
+      const bool host_only = e && e[0] == '1';
+      if (host_only || !mps_text_device(m)) {
+        m->mps_dev.release();
+        mps_host(m);
+      }
     }
+    const size_t n = m->mps_dev.p ? m->mps_dev_len : m->mps.size();
     if (!buf) {
-      *len = m->mps.size();
+      *len = n;
       return;
     }
-    if (*len < m->mps.size()) fail(XE_ERR_ARG, "buffer too small");
-    std::memcpy(buf, m->mps.data(), m->mps.size());
-    *len = m->mps.size();
+    if (*len < n) fail(XE_ERR_ARG, "buffer too small");
+    if (m->mps_dev.p) {
+      // a fresh multi-MB destination faults in page by page during the
+      // copy; ask for transparent huge pages on its aligned interior
+      const uintptr_t lo = (reinterpret_cast<uintptr_t>(buf) + kHuge - 1) & ~(kHuge - 1);
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(buf) + n) & ~(kHuge - 1);
+      if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+      XE_CUDA(cudaMemcpyAsync(buf, m->mps_dev.p, n, cudaMemcpyDeviceToHost, m->stream));
+      XE_CUDA(cudaStreamSynchronize(m->stream));
+    } else {
+      std::memcpy(buf, m->mps.data(), n);
+    }
+    *len = n;
     std::string().swap(m->mps);  // text handed out; free the cache
+    m->mps_dev.release();
   });
 }
 

@@ -26,7 +26,9 @@ struct xe_csr {
   xe::DevBuf<double> cval;
   float build_ms = 0.f;
   cudaStream_t stream = nullptr;
-  std::string mps;  // cached text (xe_write_mps two-call protocol)
+  std::string mps;  // cached host-written text (xe_write_mps two-call protocol)
+  xe::DevBuf<char> mps_dev;  // or the device-written text
+  size_t mps_dev_len = 0;
 };
 
 
@@ -47,4 +49,7 @@ struct CsrHost {
   bool quad;
 };
 std::string mps_text(const CsrHost& h);
+// device writer (mps_device.cu); false: the model needs the host writer
+bool mps_text_device(xe_csr* m);
+void mps_host(xe_csr* m);  // capi_csr.cpp
 }  // namespace xe

@@ -86,3 +86,39 @@ def test_config3_shape_and_timing():
     m = xe.build_model(prob)
     assert (m.n_rows, m.nnz, m.n_cols) == (1015581, 4348851, 659895)
     assert m.build_ms() > 0
+
+
+def _fractional_energy_doc(seed):
+    """fig2_energy with every number made non-integral: the device writer's
+    host-formatted number table must cover costs, copy costs, alpha*q, the
+    energy coefficients and limits."""
+    rng = np.random.default_rng(seed)
+    d = json.loads(golden_problem_text("fig2_energy"))
+    for op in d["operators"][1:]:
+        op["costs_ms"] = {k: float(v * rng.uniform(0.3, 3.0) + 0.1) for k, v in op["costs_ms"].items()}
+    for e in d["edges"]:
+        e["copy_ms"] = {k: float(v * rng.uniform(0.1, 2.0)) for k, v in e["copy_ms"].items()}
+    en = d["energy"]
+    en["alpha"] = float(rng.uniform(0.01, 2.0))
+    en["q_joules"] = {k: [float(x * rng.uniform(0.1, 3.0)) for x in v] for k, v in en["q_joules"].items()}
+    en["board_joules"] = float(rng.uniform(0.0, 2.0))
+    en["device_limit"] = {"gpu": float(rng.uniform(4.0, 9.0)), "cpu": float(rng.uniform(4.0, 9.0))}
+    en["total_limit"] = float(rng.uniform(10.0, 20.0))
+    return json.dumps(d)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_device_mps_equals_host_writer(seed, monkeypatch):
+    """xe_write_mps's device emitter (mps_device.cu) and the host writer
+    (mps_writer.cpp) agree byte for byte on fractional energy models (the
+    sha table above covers integral ones and ResNet-50/U-Net)."""
+    prob = xe.Problem.from_json(_fractional_energy_doc(seed))
+    for strict in (False, True):
+        for quad in (False, True):
+            opts = xe.ModelOptions(strict_free=strict, quadratic_objective=quad, energy=True)
+            monkeypatch.delenv("XE_MPS_HOST", raising=False)
+            dev = xe.build_model(prob, opts).write_mps()
+            monkeypatch.setenv("XE_MPS_HOST", "1")
+            host = xe.build_model(prob, opts).write_mps()
+            assert dev == host, (seed, strict, quad)
+            assert b"ENERGY_TOTAL" in dev
