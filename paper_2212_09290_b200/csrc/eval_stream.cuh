@@ -58,6 +58,10 @@ constexpr int kPrefetch = XE_PREFETCH;  // timesteps ahead (multi-word rows)
 #define XE_T_UNROLL 1
 #endif
 constexpr int kTUnroll = XE_T_UNROLL;  // unroll of the streaming pass over t
+#ifndef XE_PF_REG
+#define XE_PF_REG 1
+#endif
+constexpr bool kPfReg = XE_PF_REG;  // small rows: next timestep double-buffered in registers
 // multi-word rows: a smaller queue keeps two CTAs per SM within shared memory
 __host__ __device__ constexpr int qcap(int nw) { return nw == 1 ? kQCap : 128; }
 constexpr int kKindA = 1;   // full general timestep
@@ -65,7 +69,7 @@ constexpr int kKindB = 2;   // EQ11 / EQ16_HI rows of the timestep
 
 struct Job {
   uint32_t meta;  // t (bits 0..9) | owner lane (10..14) | kind (15..16)
-  uint32_t pad;
+  uint32_t next;  // the owner's next kind-A job in this queue window
   double part;    // objective part of a kind-A job (filled by the worker)
 };
 
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
     const int64_t c = g * 32 + lane;
     const uint64_t* cw = a.il + static_cast<size_t>(g) * K * 32 + lane;
     int q_cnt = 0;  // warp-uniform
+    int a_first = 0, a_last = 0, a_n = 0;  // this lane's kind-A chain in the queue
     double total = 0.0;
     int nfast = 0;
     uint64_t fzS = 0, eq12 = 0;
@@ -416,23 +421,23 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
                                              owner, &a, sm);
       }
       __syncwarp();
+      // each owner walks its own kind-A chain (push = timestep order)
       double sl = s_slow[lane];
 #pragma unroll 1
-      for (int k = 0; k < q_cnt; ++k) {
-        const Job jb = queue[k];
-        if (((jb.meta >> 10) & 31u) == static_cast<unsigned>(lane) && (jb.meta >> 15) == kKindA)
-          sl = __dadd_rn(sl, jb.part);
+      for (int k = a_first, n = a_n; n > 0; --n) {
+        sl = __dadd_rn(sl, queue[k].part);
+        k = static_cast<int>(queue[k].next);
       }
       s_slow[lane] = sl;
       __syncwarp();
       q_cnt = 0;
+      a_n = 0;
     };
 
     // rows of t in registers; t+1 prefetched for small rows
-    constexpr bool PF = MAXD * NW <= 4;
+    constexpr bool PF = kPfReg && MAXD * NW <= 4;
     uint64_t Rn[MAXD][NW], Sn[MAXD][NW];
-    auto load_t = [&](int t, uint64_t (&R)[MAXD][NW], uint64_t (&S)[MAXD][NW]) {
-      const uint64_t* pt = cw + static_cast<int64_t>(t) * NW * 32;
+    auto load_p = [&](const uint64_t* pt, uint64_t (&R)[MAXD][NW], uint64_t (&S)[MAXD][NW]) {
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
 #pragma unroll
@@ -441,7 +446,12 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
           S[d][j] = d < D ? __ldg(pt + (D + d) * dstride + j * 32) : 0ull;
         }
     };
-    if (PF) load_t(0, Rn, Sn);
+    // running pointer to the rows of the next timestep to load
+    const uint64_t* pnext = cw;
+    if (PF) {
+      load_p(pnext, Rn, Sn);
+      pnext += NW * 32;
+    }
 
 #pragma unroll kTUnroll
     for (int t = 0; t < T; ++t) {
@@ -454,12 +464,13 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
             R[d][j] = Rn[d][j];
             S[d][j] = Sn[d][j];
           }
-        if (t + 1 < T) load_t(t + 1, Rn, Sn);
+        if (t + 1 < T) load_p(pnext, Rn, Sn);
+        pnext += NW * 32;
       } else {
         // rows too wide to double-buffer in registers: prefetch the lines of
         // t + kPrefetch into L2 (no registers) while t's are loaded
         if (t + kPrefetch < T) {
-          const uint64_t* pn = cw + static_cast<int64_t>(t + kPrefetch) * NW * 32;
+          const uint64_t* pn = pnext + kPrefetch * NW * 32;
 #pragma unroll
           for (int d = 0; d < MAXD; ++d)
 #pragma unroll
@@ -469,7 +480,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + (D + d) * dstride + j * 32));
               }
         }
-        load_t(t, R, S);
+        load_p(pnext, R, S);
+        pnext += NW * 32;
       }
       const int tw = NW == 1 ? 0 : (t >> 6), tb = t & 63;
       uint64_t off = 0, eq11 = 0, zany[NW];
@@ -553,7 +565,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == kWarps ? ((MAXD * NW <= 2
       // defer the irregular timesteps
       const unsigned bA = __ballot_sync(0xffffffffu, !fast), bB = __ballot_sync(0xffffffffu, eq11 != 0);
       if (bA | bB) {
-        if (!fast) queue[q_cnt + __popc(bA & lt_mask)].meta = static_cast<uint32_t>(t) | (lane << 10) | (kKindA << 15);
+        if (!fast) {
+          const int k = q_cnt + __popc(bA & lt_mask);
+          queue[k].meta = static_cast<uint32_t>(t) | (lane << 10) | (kKindA << 15);
+          if (a_n) queue[a_last].next = static_cast<uint32_t>(k);
+          else a_first = k;
+          a_last = k;
+          ++a_n;
+        }
         const int q2 = q_cnt + __popc(bA);
         if (eq11) queue[q2 + __popc(bB & lt_mask)].meta = static_cast<uint32_t>(t - 1) | (lane << 10) | (kKindB << 15);
         q_cnt = q2 + __popc(bB);
