@@ -25,6 +25,7 @@
 // first strict minimum = lowest index among equal objective bits.
 
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "bits.cuh"
@@ -209,6 +210,164 @@ __global__ void __launch_bounds__(kWarps * 32) place_kernel(const Args a) {
   }
 }
 
+// Save-all placements, fixed-point objective, one copy cost per edge (the
+// compact tfix_edge table): the bit-sliced kernel.  A CTA takes 32
+// placements at a time, one per lane.  Phase 1 (ops, split over the warps in
+// 16-op blocks): lane k reads 16 device bytes of its placement, adds its
+// compute terms and save-all masses, and the warp ballots the device bits into
+// bit planes — plane b of op i holds bit b of dev_i of all 32 placements.
+// Phase 2 (edges, split over the warps): per edge (u, v) one broadcast
+// 8-byte load of its plane offsets and 32-bit cost, two broadcast 16-byte
+// plane loads that give the 32-placement mask of dev_u != dev_v in up to
+// three LOP3s, and each lane adds the cost when its bit is set: the per-edge
+// gathers of the warp-per-placement kernel become broadcasts.  Config 5
+// (T = 2000, E = 5987, D = 8): 82.5 -> 101 M placements/s (A/B: 16-warp
+// CTAs 93, shared atomics for the masses 91, edge costs from L1 95).
+#ifndef XE_SL_WARPS
+#define XE_SL_WARPS 8
+#endif
+constexpr int kSlWarps = XE_SL_WARPS;
+
+template <int NB>
+__global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int T = a.T, D = a.D, E = a.E;
+  uint4* planes = reinterpret_cast<uint4*>(smem);                          // [T]
+  // per edge: plane byte offsets 16 src | 16 dst << 16, and its 32-bit cost
+  uint2* s_edge = reinterpret_cast<uint2*>(planes + T);                    // [E]
+  int64_t* s_acc = reinterpret_cast<int64_t*>(s_edge + ((E + 1) & ~1));    // [warps][8][32] save-all masses
+  int64_t* s_fix = s_acc + kSlWarps * 8 * 32;                              // [warps][32]
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    s_edge[e] = make_uint2((16u * static_cast<uint32_t>(a.src[e])) | ((16u * static_cast<uint32_t>(a.dst[e])) << 16),
+                           static_cast<uint32_t>(a.tfix_edge[e]));
+  const unsigned char* pbase = reinterpret_cast<const unsigned char*>(planes);
+  const bool vec = (T % 16) == 0 && (reinterpret_cast<uintptr_t>(a.dev) % 16) == 0;
+  const int nblk = (T + 15) >> 4;
+  const int e_per = (E + kSlWarps - 1) / kSlWarps;
+  const int e0 = min(E, wid * e_per), e1 = min(E, e0 + e_per);
+  uint64_t best_key = ~0ull;
+  int64_t best_idx = -1, n_valid = 0;
+  const int64_t ngroups = (a.n + 31) / 32;
+  __syncthreads();
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int64_t c = g * 32 + lane;
+    const bool live = c < a.n;
+    const uint8_t* row = a.dev + (live ? c : 0) * T;
+    int64_t fix = 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) s_acc[(wid * 8 + x) * 32 + lane] = 0;
+    // ---- phase 1: ops
+    uint4 vnext = (vec && live && wid < nblk) ? __ldg(reinterpret_cast<const uint4*>(row) + wid) : make_uint4(0, 0, 0, 0);
+    for (int b = wid; b < nblk; b += kSlWarps) {
+      uint32_t wv[4];
+      if (vec) {
+        // the next block's bytes are in flight while this block is processed
+        const uint4 v = vnext;
+        if (live && b + kSlWarps < nblk) vnext = __ldg(reinterpret_cast<const uint4*>(row) + b + kSlWarps);
+        wv[0] = v.x;
+        wv[1] = v.y;
+        wv[2] = v.z;
+        wv[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const int i = 16 * b + 4 * q + y;
+            if (live && i < T) x |= static_cast<uint32_t>(row[i]) << (8 * y);
+          }
+          wv[q] = x;
+        }
+      }
+      const int jn = min(16, T - 16 * b);  // warp-uniform
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < jn) {
+          const int i = 16 * b + j;
+          const int d = static_cast<int>((wv[j >> 2] >> (8 * (j & 3))) & 0xffu);
+          const unsigned p0 = __ballot_sync(0xffffffffu, d & 1);
+          const unsigned p1 = NB > 1 ? __ballot_sync(0xffffffffu, (d >> 1) & 1) : 0u;
+          const unsigned p2 = NB > 2 ? __ballot_sync(0xffffffffu, (d >> 2) & 1) : 0u;
+          if (lane == 0) planes[i] = make_uint4(p0, p1, p2, 0u);
+          fix += __ldg(a.tfix + d * T + i);
+          s_acc[(wid * 8 + d) * 32 + lane] += __ldg(a.mass + i);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: edges
+#pragma unroll 4
+    for (int e = e0; e < e1; ++e) {
+      const uint2 ed = s_edge[e];
+      const uint32_t sd = ed.x;
+      const uint4 pu = *reinterpret_cast<const uint4*>(pbase + (sd & 0xffffu));
+      const uint4 pv = *reinterpret_cast<const uint4*>(pbase + (sd >> 16));
+      unsigned diff = pu.x ^ pv.x;
+      if (NB > 1) diff |= pu.y ^ pv.y;
+      if (NB > 2) diff |= pu.z ^ pv.z;
+      if ((diff >> lane) & 1u) fix += static_cast<int32_t>(ed.y);
+    }
+    s_fix[wid * 32 + lane] = fix;
+    __syncthreads();
+    // ---- warp 0: totals, flags, outputs
+    if (wid == 0) {
+      int64_t f = 0;
+#pragma unroll
+      for (int w = 0; w < kSlWarps; ++w) f += s_fix[w * 32 + lane];
+      const double obj = ldexp(static_cast<double>(f), -a.fix_k);
+      uint32_t fl = 0;
+      int64_t pk[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        int64_t v = 0;
+#pragma unroll
+        for (int w = 0; w < kSlWarps; ++w) v += s_acc[(w * 8 + x) * 32 + lane];
+        pk[x] = v;
+        if (x < D) {
+          if (v > a.budget[x]) fl |= XE_F_BUDGET;
+          if (static_cast<double>(v) > a.ubound[x]) fl |= XE_F_U_BOUND;
+        }
+      }
+      if (live) {
+        if (a.obj) a.obj[c] = obj;
+        if (a.flags) a.flags[c] = fl;
+        if (a.peak)
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+            if (x < D) a.peak[c * D + x] = pk[x];
+        if ((fl & a.valid_mask) == 0) {
+          ++n_valid;
+          const uint64_t key = __double_as_longlong(obj);
+          if (key < best_key || (key == best_key && c < best_idx)) {
+            best_key = key;
+            best_idx = c;
+          }
+        }
+      }
+    }
+    __syncthreads();  // planes, accumulators and partial sums are reused
+  }
+  if (wid == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, best_key, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, best_idx, o);
+      if (ok < best_key || (ok == best_key && oi >= 0 && (best_idx < 0 || oi < best_idx))) {
+        best_key = ok;
+        best_idx = oi;
+      }
+    }
+    const int64_t nv = warp_sum_i64(n_valid);
+    if (lane == 0) {
+      a.wbest_key[blockIdx.x] = best_key;
+      a.wbest_idx[blockIdx.x] = best_idx;
+      a.wvalid[blockIdx.x] = nv;
+    }
+  }
+}
+
 // ---- assignment oracle: thread per odometer index -------------------------
 struct OracleArgs {
   int D, T, E;
@@ -323,6 +482,7 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   // copy cost uniform over device pairs per edge (a single link model, the
   // config-5 generator): the compact per-edge table
   DevBuf<int64_t> tedge;
+  bool tedge32 = false;
   if (pr->fix_k_place >= 0 && h.D > 1) {
     bool uniform = true;
     std::vector<int64_t> te(static_cast<size_t>(h.E));
@@ -339,6 +499,7 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
     if (uniform && h.E > 0) {
       tedge.upload(te, s);
       a.tfix_edge = tedge.p;
+      tedge32 = std::all_of(te.begin(), te.end(), [](int64_t v) { return v >= INT32_MIN && v <= INT32_MAX; });
     }
   }
   a.src = pr->d_src.p;
@@ -363,6 +524,41 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   a.wvalid = reinterpret_cast<int64_t*>(scratch + nw_max * 16);
   const int tb = (h.T + 15) & ~15;
   if (h.T > 65535) fail(XE_ERR_TOO_LARGE, "placement evaluation supports T <= 65535");
+  const char* sl_env = std::getenv("XE_PLACE_SLICED");
+  if (policy == 0 && a.tfix_edge && tedge32 && h.T <= 4095 && !(sl_env && sl_env[0] == '0')) {
+    // bit-sliced save-all kernel (one lane per placement)
+    const size_t smem_sl = static_cast<size_t>(h.T) * 16 + static_cast<size_t>((h.E + 1) & ~1) * 8 +
+                           static_cast<size_t>(place::kSlWarps) * (8 * 32 * 8 + 32 * 8);
+    int dev_smem = 0;
+    XE_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
+    if (smem_sl <= static_cast<size_t>(dev_smem)) {
+      auto ks = h.D <= 2 ? place::place_sliced_kernel<1> : h.D <= 4 ? place::place_sliced_kernel<2>
+                                                                     : place::place_sliced_kernel<3>;
+      XE_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_sl)));
+      int per_sm = 0;
+      XE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, place::kSlWarps * 32, smem_sl));
+      const int64_t groups = (n + 31) / 32;
+      // one best slot per CTA; the scratch holds nsm * 64 slots
+      const int grid = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(groups, static_cast<int64_t>(nsm) * std::max(1, std::min(per_sm, 8)))));
+      if (n > 0) {
+        ks<<<grid, place::kSlWarps * 32, smem_sl, s>>>(a);
+        XE_CUDA(cudaGetLastError());
+      }
+      if (best3) {
+        extern void reduce_best_launch(const uint64_t* key, const int64_t* idx, const int64_t* valid, int n,
+                                       uint64_t* out, cudaStream_t s);
+        if (n > 0) {
+          reduce_best_launch(a.wbest_key, a.wbest_idx, a.wvalid, grid, best3, s);
+        } else {
+          const uint64_t none[3] = {~0ull, ~0ull, 0ull};
+          XE_CUDA(cudaMemcpyAsync(best3, none, sizeof none, cudaMemcpyHostToDevice, s));
+        }
+      }
+      XE_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+  }
   const int smem = ((4 * h.E + 15) & ~15) + place::kWarps * tb + place::kWarps * 8 * 32 * 8;
   const bool exact = pr->fix_k_place >= 0;
   auto k = exact ? place::place_kernel<true> : place::place_kernel<false>;
