@@ -32,11 +32,15 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
 
 #include "csr.hpp"
 
@@ -186,6 +190,15 @@ struct SellView {
   int64_t len, nlong, ns;
 };
 
+// Coded entries: when the unscaled matrix holds at most 256 distinct values
+// and both dimensions are below 2^24 (the K1 models: 15-25 values), an entry
+// is one 32-bit word, index | code << 24, and the value is the code's entry
+// of a 256-double table in shared memory; the scaling moves to the vectors,
+// (Dr K Dc) x = Dr (K (Dc x)).  4 bytes per entry instead of 12.
+constexpr int kCodeShift = 24;
+constexpr uint32_t kIdxMask = (1u << kCodeShift) - 1u;
+constexpr int kMaxCodes = 256;
+
 __global__ void sort_key_kernel(const int64_t* p, int64_t n, int kLong, uint32_t* key, int32_t* iota,
                                 unsigned long long* nlong) {
   GRID_LOOP(i, n) {
@@ -219,21 +232,37 @@ __global__ void sell_size_kernel(const int32_t* slen, int64_t len, int64_t nlong
     sz[k] = v;
   }
 }
+// code of value x in the sorted table vt[0, nvt) (x is present)
+__device__ __forceinline__ uint32_t code_of(const double* vt, int nvt, double x) {
+  int lo = 0, hi = nvt - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (vt[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return static_cast<uint32_t>(lo) << kCodeShift;
+}
+
 __global__ void sell_fill_kernel(const int64_t* p, const int32_t* idx_in, const double* v_in, const int32_t* perm,
                                  const int32_t* remap, int64_t len, int64_t nlong, int64_t ns, const int64_t* ptr,
-                                 int32_t* idx, double* v) {
+                                 int32_t* idx, double* v, const double* vt, int nvt) {
+  // coded: idx = index | code << 24, no value array
+  const uint32_t zcode = vt ? code_of(vt, nvt, 0.0) : 0u;
+  auto put = [&](int64_t at, bool in, int64_t q) {
+    if (vt) {
+      idx[at] = in ? static_cast<int32_t>(static_cast<uint32_t>(remap[idx_in[q]]) | code_of(vt, nvt, v_in[q]))
+                   : static_cast<int32_t>(zcode);
+    } else {
+      idx[at] = in ? remap[idx_in[q]] : 0;
+      v[at] = in ? v_in[q] : 0.0;
+    }
+  };
   GRID_LOOP(k, nlong + ns * 32) {
     if (k < nlong) {
       const int32_t i = perm[k];
       const int64_t q0 = p[i], l = p[i + 1] - q0, o = ptr[k];
-      for (int64_t t = 0; t < l; ++t) {
-        idx[o + t] = remap[idx_in[q0 + t]];
-        v[o + t] = v_in[q0 + t];
-      }
-      if (l & 1) {  // the even padding entry: 0 * x[0]
-        idx[o + l] = 0;
-        v[o + l] = 0.0;
-      }
+      for (int64_t t = 0; t < l; ++t) put(o + t, true, q0 + t);
+      if (l & 1) put(o + l, false, 0);  // the even padding entry: 0 * x[0]
       continue;
     }
     const int64_t r = k - nlong, sl = r >> 5, row = k;
@@ -251,8 +280,7 @@ __global__ void sell_fill_kernel(const int64_t* p, const int32_t* idx_in, const 
     for (int64_t t = 0; t < w; ++t) {
       const bool in = t < l;
       const int64_t at = base + 64 * (t >> 1) + 2 * lane + (t & 1);
-      idx[at] = in ? remap[idx_in[q0 + t]] : 0;
-      v[at] = in ? v_in[q0 + t] : 0.0;
+      put(at, in, q0 + t);
     }
   }
 }
@@ -305,15 +333,17 @@ void sell_plan(const int64_t* p, int64_t n, int long_min, Sell& S, cudaStream_t 
   XE_CUDA(cudaStreamSynchronize(s));  // temporaries freed on return
 }
 
-// fill from CSR/CSC (p, idx, v), indices remapped by `remap`
-void sell_fill(const int64_t* p, const int32_t* idx, const double* v, const int32_t* remap, Sell& S, cudaStream_t s) {
+// fill from CSR/CSC (p, idx, v), indices remapped by `remap`; coded when
+// vt (the sorted distinct values of v, 0 included) is given
+void sell_fill(const int64_t* p, const int32_t* idx, const double* v, const int32_t* remap, Sell& S, cudaStream_t s,
+               const double* vt = nullptr, int nvt = 0) {
   int64_t total = 0;
   XE_CUDA(cudaMemcpyAsync(&total, S.sptr.p + S.nlong + S.ns + 1, 8, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaStreamSynchronize(s));
   S.idx.alloc(std::max<int64_t>(1, total));
-  S.v.alloc(std::max<int64_t>(1, total));
+  S.v.alloc(vt ? 1 : std::max<int64_t>(1, total));
   sell_fill_kernel<<<grid(S.nlong + S.ns * 32), kB, 0, s>>>(p, idx, v, S.perm.p, remap, S.len, S.nlong, S.ns,
-                                                            S.sptr.p, S.idx.p, S.v.p);
+                                                            S.sptr.p, S.idx.p, S.v.p, vt, nvt);
   XE_CUDA(cudaGetLastError());
 }
 
@@ -325,16 +355,25 @@ __device__ __forceinline__ double warp_sum(double a) {
   return a;
 }
 
-// dot product of long row w with x, complete on every lane
-__device__ __forceinline__ double long_dot(const SellView& A, int64_t w, const double* __restrict__ x, int lane) {
+// dot product of long row w with x, complete on every lane (CODED: values
+// from the shared table vt)
+template <bool CODED>
+__device__ __forceinline__ double long_dot(const SellView& A, int64_t w, const double* __restrict__ x, int lane,
+                                           const double* vt) {
   const int64_t b = A.ptr[w], e = A.ptr[w + 1];
   double acc = 0.0;
-  for (int64_t q = b + lane; q < e; q += 32) acc += __ldg(A.v + q) * __ldg(x + __ldg(A.idx + q));
+  for (int64_t q = b + lane; q < e; q += 32) {
+    const uint32_t ix = static_cast<uint32_t>(__ldg(A.idx + q));
+    if (CODED) acc += vt[ix >> kCodeShift] * __ldg(x + (ix & kIdxMask));
+    else acc += __ldg(A.v + q) * __ldg(x + ix);
+  }
   return warp_sum(acc);
 }
 
 // dot product of this lane's row of slice sl with x
-__device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const double* __restrict__ x, int lane) {
+template <bool CODED>
+__device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const double* __restrict__ x, int lane,
+                                            const double* vt) {
   const int64_t base = A.ptr[A.nlong + 1 + sl];
   const int w2 = static_cast<int>((A.ptr[A.nlong + 2 + sl] - base) >> 6);  // entry pairs
   const int2* ip = reinterpret_cast<const int2*>(A.idx + base) + lane;
@@ -343,11 +382,23 @@ __device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const
 #pragma unroll 2
   for (int t = 0; t < w2; ++t) {
     const int2 ix = __ldg(ip + 32 * t);
-    const double2 vv = __ldg(vp + 32 * t);
-    acc += vv.x * __ldg(x + ix.x);
-    acc += vv.y * __ldg(x + ix.y);
+    if (CODED) {
+      const uint32_t a0 = static_cast<uint32_t>(ix.x), a1 = static_cast<uint32_t>(ix.y);
+      acc += vt[a0 >> kCodeShift] * __ldg(x + (a0 & kIdxMask));
+      acc += vt[a1 >> kCodeShift] * __ldg(x + (a1 & kIdxMask));
+    } else {
+      const double2 vv = __ldg(vp + 32 * t);
+      acc += vv.x * __ldg(x + ix.x);
+      acc += vv.y * __ldg(x + ix.y);
+    }
   }
   return acc;
+}
+
+// the value table into shared memory (CODED kernels)
+__device__ __forceinline__ void load_codes(double* s_vt, const double* vt) {
+  for (int i = threadIdx.x; i < kMaxCodes; i += blockDim.x) s_vt[i] = vt[i];
+  __syncthreads();
 }
 
 #define WARP_ITEMS(w, A)                                                                                 \
@@ -356,18 +407,29 @@ __device__ __forceinline__ double slice_dot(const SellView& A, int64_t sl, const
   for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < (A).nlong + (A).ns; \
        w += nw_)
 
-// out = A x (rows of A in reordered order)
-__global__ void sell_spmv_kernel(SellView A, const double* __restrict__ x, double* __restrict__ out) {
+// out = A x (rows of A in reordered order).  Coded: out = Dout (A x) with x
+// already multiplied by the input scaling (scale_into_kernel): the scaled
+// matrix applied through the unscaled codes.
+template <bool CODED>
+__global__ void sell_spmv_kernel(SellView A, const double* __restrict__ x, double* __restrict__ out,
+                                 const double* __restrict__ vt, const double* __restrict__ dout) {
+  __shared__ double s_vt[kMaxCodes];
+  if (CODED) load_codes(s_vt, vt);
   WARP_ITEMS(w, A) {
     if (w < A.nlong) {
-      const double acc = long_dot(A, w, x, lane);
-      if (lane == 0) out[w] = acc;
+      const double acc = long_dot<CODED>(A, w, x, lane, s_vt);
+      if (lane == 0) out[w] = CODED ? acc * dout[w] : acc;
     } else {
       const int64_t sl = w - A.nlong, k = A.nlong + sl * 32 + lane;
-      const double acc = slice_dot(A, sl, x, lane);
-      if (k < A.len) out[k] = acc;
+      const double acc = slice_dot<CODED>(A, sl, x, lane, s_vt);
+      if (k < A.len) out[k] = CODED ? acc * dout[k] : acc;
     }
   }
+}
+
+// xs = D x (the input of a coded product)
+__global__ void scale_into_kernel(const double* x, const double* D, int64_t n, double* xs) {
+  GRID_LOOP(i, n) xs[i] = x[i] * D[i];
 }
 
 struct Iter {
@@ -378,6 +440,9 @@ struct Iter {
   const double *x0, *y0;           // anchor: the last restart point
   const double* step;              // device [tau, sigma, k of the block's first iteration]
   int64_t m, n;
+  // coded: value table, scalings, the scaled vectors the products gather
+  const double *vt, *Dr, *Dc;
+  double *yD, *xbarD;  // Dr y and Dc xbar
 };
 
 // Reflected Halpern PDHG (restarted): with T the PDHG operator
@@ -412,7 +477,10 @@ __device__ __forceinline__ void pdl_enter() {
   cudaTriggerProgrammaticLaunchCompletion();
 }
 
+template <bool CODED>
 __global__ void __launch_bounds__(kB) primal_sell_kernel(Iter it, int jk) {
+  __shared__ double s_vt[kMaxCodes];
+  if (CODED) load_codes(s_vt, it.vt);  // constant: before the dependency wait
   pdl_enter();
   const double tau = it.step[0];
   double ha, hb;
@@ -423,26 +491,33 @@ __global__ void __launch_bounds__(kB) primal_sell_kernel(Iter it, int jk) {
     const int64_t j = lg ? w : it.C.nlong + sl * 32 + lane;
     const bool on = lg ? lane == 0 : j < it.n;
     // per-column operands first, so their loads overlap the dot product
-    double cj = 0.0, xj = 0.0, lo = 0.0, hi = 0.0, x0 = 0.0;
+    double cj = 0.0, xj = 0.0, lo = 0.0, hi = 0.0, x0 = 0.0, dc = 1.0;
     if (on) {
       cj = __ldg(it.c + j);
       lo = __ldg(it.lb + j);
       hi = __ldg(it.ub + j);
       x0 = __ldg(it.x0 + j);
       xj = it.x[j];
+      if (CODED) dc = __ldg(it.Dc + j);
     }
-    const double acc = lg ? long_dot(it.C, w, it.y, lane) : slice_dot(it.C, sl, it.y, lane);
+    const double* yv = CODED ? it.yD : it.y;
+    double acc = lg ? long_dot<CODED>(it.C, w, yv, lane, s_vt) : slice_dot<CODED>(it.C, sl, yv, lane, s_vt);
     if (on) {
+      if (CODED) acc *= dc;
       const double xt = fmin(fmax(xj - tau * (cj - acc), lo), hi);
       const double xb = 2.0 * xt - xj;
       it.xt[j] = xt;
-      it.xbar[j] = xb;
+      if (CODED) it.xbarD[j] = dc * xb;
+      else it.xbar[j] = xb;
       it.x[j] = ha * xb + hb * x0;
     }
   }
 }
 
+template <bool CODED>
 __global__ void __launch_bounds__(kB) dual_sell_kernel(Iter it, int jk) {
+  __shared__ double s_vt[kMaxCodes];
+  if (CODED) load_codes(s_vt, it.vt);
   pdl_enter();
   const double sigma = it.step[1];
   double ha, hb;
@@ -452,19 +527,24 @@ __global__ void __launch_bounds__(kB) dual_sell_kernel(Iter it, int jk) {
     const int64_t sl = w - it.R.nlong;
     const int64_t i = lg ? w : it.R.nlong + sl * 32 + lane;
     const bool on = lg ? lane == 0 : i < it.m;
-    double bi = 0.0, yi = 0.0, y0 = 0.0;
+    double bi = 0.0, yi = 0.0, y0 = 0.0, dr = 1.0;
     int8_t sn = 'E';
     if (on) {
       bi = __ldg(it.b + i);
       sn = __ldg(it.sense + i);
       y0 = __ldg(it.y0 + i);
       yi = it.y[i];
+      if (CODED) dr = __ldg(it.Dr + i);
     }
-    const double acc = lg ? long_dot(it.R, w, it.xbar, lane) : slice_dot(it.R, sl, it.xbar, lane);
+    const double* xv = CODED ? it.xbarD : it.xbar;
+    double acc = lg ? long_dot<CODED>(it.R, w, xv, lane, s_vt) : slice_dot<CODED>(it.R, sl, xv, lane, s_vt);
     if (on) {
+      if (CODED) acc *= dr;
       const double yt = dual_proj(yi + sigma * (bi - acc), sn);
+      const double yn = ha * (2.0 * yt - yi) + hb * y0;
       it.yt[i] = yt;
-      it.y[i] = ha * (2.0 * yt - yi) + hb * y0;
+      it.y[i] = yn;
+      if (CODED) it.yD[i] = dr * yn;
     }
   }
 }
@@ -564,7 +644,7 @@ using namespace pd;
 
 struct PdhgState {
   DevBuf<double> Dr, Dr0, Dc, c_fix, ub_fix, val_s, cval_s, c_s, lb_s, ub_s, b_s, x, xbar, xt, y, yt, x0, y0, Kx, Kty, xa, ya, part,
-      step, tmpn, tmpm;
+      step, tmpn, tmpm, vt, yD, xbarD, xsn, xsm;
   DevBuf<int32_t> col_of;
 };
 
@@ -574,13 +654,45 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   build_csc(M, s);
   const int64_t m = M->info.n_rows, n = M->info.n_cols, nnz = M->info.nnz;
   PdhgState S;
+  // coded entries when the matrix has few distinct values (kMaxCodes, 0 included)
+  int nvt = 0;
+  {
+    const char* e = std::getenv("XE_PDHG_CODED");
+    const bool allow = !(e && e[0] == '0');
+    // (small models are latency-bound: VGG-16 7.2 vs 7.6 us/iteration coded;
+    // ResNet-50 cfg 3 51.2 -> 43.1, U-Net cfg 4 56.0 -> 45.5)
+    if (allow && nnz >= (1ll << 20) && m < (1ll << kCodeShift) && n < (1ll << kCodeShift)) {
+      DevBuf<double> u;
+      u.alloc(static_cast<size_t>(nnz) + 1);
+      XE_CUDA(cudaMemcpyAsync(u.p, M->val.p, nnz * 8, cudaMemcpyDeviceToDevice, s));
+      const double zero = 0.0;
+      XE_CUDA(cudaMemcpyAsync(u.p + nnz, &zero, 8, cudaMemcpyHostToDevice, s));
+      thrust::sort(thrust::cuda::par.on(s), u.p, u.p + nnz + 1);
+      const int64_t nu = thrust::unique(thrust::cuda::par.on(s), u.p, u.p + nnz + 1) - u.p;
+      if (nu <= kMaxCodes) {
+        std::vector<double> h(static_cast<size_t>(nu));
+        XE_CUDA(cudaMemcpyAsync(h.data(), u.p, nu * 8, cudaMemcpyDeviceToHost, s));
+        XE_CUDA(cudaStreamSynchronize(s));
+        nvt = static_cast<int>(nu);
+        h.resize(kMaxCodes, h.back());  // table padded to the shared copy's size
+        S.vt.upload(h, s);
+      }
+    }
+  }
+  const bool coded = nvt > 0;
   S.Dr.alloc(m);
   S.Dr0.alloc(m);
   S.Dc.alloc(n);
   S.c_fix.alloc(n);
   S.ub_fix.alloc(n);
-  S.val_s.alloc(nnz);
-  S.cval_s.alloc(nnz);
+  S.val_s.alloc(coded ? 1 : nnz);
+  S.cval_s.alloc(coded ? 1 : nnz);
+  if (coded) {
+    S.yD.alloc(m);
+    S.xbarD.alloc(n);
+    S.xsn.alloc(n);
+    S.xsm.alloc(m);
+  }
   S.c_s.alloc(n);
   S.lb_s.alloc(n);
   S.ub_s.alloc(n);
@@ -625,8 +737,10 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
       rescale_kernel<<<grid(m), kB, 0, s>>>(S.Dr.p, S.tmpm.p, m);
       rescale_kernel<<<grid(n), kB, 0, s>>>(S.Dc.p, S.tmpn.p, n);
     }
-    scale_csr_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->col.p, M->val.p, S.Dr.p, S.Dc.p, m, S.val_s.p);
-    scale_csc_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, M->cval.p, S.Dr.p, S.Dc.p, n, S.cval_s.p);
+    if (!coded) {
+      scale_csr_kernel<<<grid(m), kB, 0, s>>>(M->row_ptr.p, M->col.p, M->val.p, S.Dr.p, S.Dc.p, m, S.val_s.p);
+      scale_csc_kernel<<<grid(n), kB, 0, s>>>(M->col_ptr.p, M->crow.p, M->cval.p, S.Dr.p, S.Dc.p, n, S.cval_s.p);
+    }
     sentinel_kernel<<<grid(n), kB, 0, s>>>(M->obj.p, lb, ub, n, S.c_fix.p, S.ub_fix.p, fixcnt.p);
     scale_vec_kernel<<<grid(n), kB, 0, s>>>(S.c_fix.p, lb, S.ub_fix.p, S.Dc.p, n, S.c_s.p, S.lb_s.p, S.ub_s.p);
     scale_b_kernel<<<grid(m), kB, 0, s>>>(M->rhs.p, S.Dr.p, m, S.b_s.p);
@@ -646,8 +760,13 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   Sell R, C;
   sell_plan(M->row_ptr.p, m, long_threshold(m), R, s);
   sell_plan(M->col_ptr.p, n, long_threshold(n), C, s);
-  sell_fill(M->row_ptr.p, M->col.p, S.val_s.p, C.inv.p, R, s);
-  sell_fill(M->col_ptr.p, M->crow.p, S.cval_s.p, R.inv.p, C, s);
+  if (coded) {
+    sell_fill(M->row_ptr.p, M->col.p, M->val.p, C.inv.p, R, s, S.vt.p, nvt);
+    sell_fill(M->col_ptr.p, M->crow.p, M->cval.p, R.inv.p, C, s, S.vt.p, nvt);
+  } else {
+    sell_fill(M->row_ptr.p, M->col.p, S.val_s.p, C.inv.p, R, s);
+    sell_fill(M->col_ptr.p, M->crow.p, S.cval_s.p, R.inv.p, C, s);
+  }
   auto permute = [&](DevBuf<double>& v, const Sell& P, DevBuf<double>& tmp) {
     gather_kernel<double><<<grid(P.len), kB, 0, s>>>(v.p, P.perm.p, P.len, tmp.p);
     XE_CUDA(cudaMemcpyAsync(v.p, tmp.p, P.len * 8, cudaMemcpyDeviceToDevice, s));
@@ -667,10 +786,20 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   S.val_s.release();
   S.cval_s.release();
   auto Kmul = [&](const double* xv, double* out) {  // out = K~ x (sorted rows)
-    sell_spmv_kernel<<<items_grid(R), kB, 0, s>>>(view(R), xv, out);
+    if (coded) {
+      scale_into_kernel<<<grid(n), kB, 0, s>>>(xv, S.Dc.p, n, S.xsn.p);
+      sell_spmv_kernel<true><<<items_grid(R), kB, 0, s>>>(view(R), S.xsn.p, out, S.vt.p, S.Dr.p);
+    } else {
+      sell_spmv_kernel<false><<<items_grid(R), kB, 0, s>>>(view(R), xv, out, nullptr, nullptr);
+    }
   };
   auto KTmul = [&](const double* yv, double* out) {  // out = K~' y (sorted columns)
-    sell_spmv_kernel<<<items_grid(C), kB, 0, s>>>(view(C), yv, out);
+    if (coded) {
+      scale_into_kernel<<<grid(m), kB, 0, s>>>(yv, S.Dr.p, m, S.xsm.p);
+      sell_spmv_kernel<true><<<items_grid(C), kB, 0, s>>>(view(C), S.xsm.p, out, S.vt.p, S.Dc.p);
+    } else {
+      sell_spmv_kernel<false><<<items_grid(C), kB, 0, s>>>(view(C), yv, out, nullptr, nullptr);
+    }
   };
   auto sqdist = [&](const double* a, const double* b, int64_t len) {
     const int g = grid(len);
@@ -712,6 +841,7 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   // ---- state
   XE_CUDA(cudaMemsetAsync(S.x.p, 0, n * 8, s));
   XE_CUDA(cudaMemsetAsync(S.y.p, 0, m * 8, s));
+  if (coded) XE_CUDA(cudaMemsetAsync(S.yD.p, 0, m * 8, s));
   XE_CUDA(cudaMemsetAsync(S.xt.p, 0, n * 8, s));
   XE_CUDA(cudaMemsetAsync(S.yt.p, 0, m * 8, s));
   XE_CUDA(cudaMemsetAsync(S.x0.p, 0, n * 8, s));  // anchor = last restart point
@@ -741,6 +871,11 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   it.step = S.step.p;
   it.m = m;
   it.n = n;
+  it.vt = S.vt.p;
+  it.Dr = S.Dr.p;
+  it.Dc = S.Dc.p;
+  it.yD = S.yD.p;
+  it.xbarD = S.xbarD.p;
 
   const int block = o.check_every > 0 ? o.check_every : 64;
   // captured graph of `block` iterations
@@ -761,8 +896,13 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   };
   XE_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < block; ++k) {
-    launch(primal_sell_kernel, items_grid(C), k);
-    launch(dual_sell_kernel, items_grid(R), k);
+    if (coded) {
+      launch(primal_sell_kernel<true>, items_grid(C), k);
+      launch(dual_sell_kernel<true>, items_grid(R), k);
+    } else {
+      launch(primal_sell_kernel<false>, items_grid(C), k);
+      launch(dual_sell_kernel<false>, items_grid(R), k);
+    }
   }
   XE_CUDA(cudaStreamEndCapture(s, &graph));
   XE_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
@@ -840,6 +980,7 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
       if (dx > 1e-10 && dy > 1e-10) omega = std::exp(0.5 * std::log(dy / dx) + 0.5 * std::log(omega));
       for (auto* v : {&S.x, &S.x0}) XE_CUDA(cudaMemcpyAsync(v->p, S.xt.p, n * 8, cudaMemcpyDeviceToDevice, s));
       for (auto* v : {&S.y, &S.y0}) XE_CUDA(cudaMemcpyAsync(v->p, S.yt.p, m * 8, cudaMemcpyDeviceToDevice, s));
+      if (coded) scale_into_kernel<<<grid(m), kB, 0, s>>>(S.yt.p, S.Dr.p, m, S.yD.p);
       last_restart = cur;
       since = 0;
       ++restarts;
