@@ -142,6 +142,16 @@ def _event_ms(fn, reps=3, warmup=1, stream=None):
     return e0.elapsed_time(e1) / reps, r
 
 
+def pdhg_iter_bytes(model, lp):
+    """Algorithmic HBM bytes of one PDHG iteration (both half-steps): the two
+    sliced matrices (coded: one 4-byte word per entry; else an index and an
+    fp64 value, 12 bytes) plus the per-column / per-row operand and result
+    vectors (coded adds the scalings and the scaled copies the products gather)."""
+    if lp.coded:
+        return 8 * model.nnz + 72 * model.n_cols + 57 * model.n_rows
+    return 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
+
+
 def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
     """One dense-cube config (3 ResNet-50 / 4 U-Net) on one GPU: K1 model, K3
     PDHG to 1e-7 (HBM roofline of the half-steps), K4 LP-guided rounding and
@@ -152,7 +162,7 @@ def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
     k1_wall, model = _timed(lambda: xe.build_model(prob), warmup=1, reps=1)
     mps_wall, mps_len = _timed(lambda: len(model.write_mps()), warmup=1, reps=3)
     lp = xe.pdhg_solve(model, tol=1e-7, max_iters=1000000, return_x=True)
-    it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
+    it_bytes = pdhg_iter_bytes(model, lp)
     x = torch.from_numpy(lp.x).cuda()
     gen_ms, cubes = _event_ms(lambda: xe.round_cubes(prob, n, SEED, edits=3, perturb=0.0, x=x), reps=1)
     il = xe.cubes_to_il(prob, cubes)
@@ -173,6 +183,7 @@ def dense_config(name, doc_fn, n, hbm, want_lp=None, highs_recorded=None):
                   "iters_per_s": lp.iters / (lp.solve_ms / 1e3), "time_to_tol_ms": lp.solve_ms, "tol": 1e-7,
                   "objective": lp.primal_obj, "dual_bound": lp.dual_obj,
                   "roofline": {"bound": "hbm", "bytes_per_iter": it_bytes,
+                               "entries": "coded (4 B)" if lp.coded else "fp64 (12 B)",
                                "achieved": it_bytes / (lp.ms_per_iter / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                "frac": it_bytes / (lp.ms_per_iter / 1e3) / 1e9 / hbm}},
          "k4_rounding": {"candidates": n, "candidates_per_s": n / (gen_ms / 1e3)},
@@ -318,7 +329,7 @@ def resnet_pipeline(args):
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
+    it_bytes = pdhg_iter_bytes(model, lp)
     hbm = peaks()[0]
     bpc = prob.cube_words * 4 + 8 + 8 * prob.D + 4
     line = {"metric": METRIC, "value": n / (ms / 1e3), "unit": "candidates/s", "n_gpus": 1, "steps": args.steps,
@@ -614,7 +625,7 @@ def main():
         k1_bytes = 12 * model.nnz + 8 * (model.n_rows + 1) + 26 * model.n_cols
         lp = xe.pdhg_solve(model, tol=1e-7, max_iters=400000)
         want = 118.68224203657523  # HiGHS 1.12.0 on the reference MPS (tests/golden/lp_values.json)
-        it_bytes = 24 * model.nnz + 64 * model.n_cols + 41 * model.n_rows
+        it_bytes = pdhg_iter_bytes(model, lp)
         line["k1_build"] = {"rows": model.n_rows, "cols": model.n_cols, "nnz": model.nnz, "ms": build_ms,
                             "achieved_gbs": k1_bytes / (build_ms / 1e3) / 1e9 if build_ms > 0 else None}
         line["pdhg"] = {

@@ -318,6 +318,10 @@ typedef struct xe_pdhg_result {
    * final duals price every fixed column non-negatively (reduced cost
    * 1e9 - K'y >= 0), i.e. the fixing provably left the LP optimum unchanged */
   int32_t presolve_fixed, certified;
+  /* 1 when the half-steps ran on coded entries (<= 256 distinct matrix
+   * values: 4 bytes per entry, scaling applied to the vectors), 0 on
+   * scaled fp64 values (12 bytes per entry) */
+  int32_t coded_entries;
 } xe_pdhg_result;
 
 int xe_pdhg_solve(xe_csr* m, const xe_pdhg_opts* opts, xe_pdhg_result* res,

@@ -109,7 +109,7 @@ class PdhgResult(C.Structure):
                 ("rel_dual_res", C.c_double), ("iters", C.c_int32),
                 ("restarts", C.c_int32), ("status", C.c_int32),
                 ("solve_ms", C.c_double), ("spmv_ms_per_iter", C.c_double),
-                ("presolve_fixed", C.c_int32), ("certified", C.c_int32)]
+                ("presolve_fixed", C.c_int32), ("certified", C.c_int32), ("coded_entries", C.c_int32)]
 
 
 class SearchOpts(C.Structure):

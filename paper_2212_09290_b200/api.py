@@ -461,6 +461,7 @@ class LpResult:
     ms_per_iter: float
     presolve_fixed: int = 0
     certified: bool = True
+    coded: bool = False  # half-steps on coded entries (4 B) instead of fp64 values (12 B)
     x: Optional[np.ndarray] = None
     y: Optional[np.ndarray] = None
 
@@ -480,7 +481,8 @@ def pdhg_solve(model: Model, tol: float = 1e-6, max_iters: int = 200000, check_e
     check(LIB.xe_pdhg_solve(model.handle, C.byref(o), C.byref(r),
                             None if x is None else x.ctypes.data, None if y is None else y.ctypes.data))
     return LpResult(r.primal_obj, r.dual_obj, r.rel_gap, r.rel_primal_res, r.iters, r.restarts,
-                    r.status == 0, r.solve_ms, r.spmv_ms_per_iter, r.presolve_fixed, bool(r.certified), x, y)
+                    r.status == 0, r.solve_ms, r.spmv_ms_per_iter, r.presolve_fixed, bool(r.certified),
+                    bool(r.coded_entries), x, y)
 
 
 def build_model(problem: "Problem", opts: Optional[ModelOptions] = None) -> Model:

@@ -1008,6 +1008,7 @@ void pdhg_solve(xe_csr* M, const xe_pdhg_opts& o, xe_pdhg_result* res, double* x
   XE_CUDA(cudaMemcpyAsync(fc, fixcnt.p, 16, cudaMemcpyDeviceToHost, s));
   XE_CUDA(cudaStreamSynchronize(s));
   res->presolve_fixed = static_cast<int32_t>(fc[0]);
+  res->coded_entries = coded ? 1 : 0;
   res->certified = fc[1] == 0 ? 1 : 0;
   res->primal_obj = cur.pobj;
   res->dual_obj = cur.dobj;
