@@ -106,7 +106,8 @@ typedef struct xe_problem_desc {
   const double* cost_ms;       /* [D][T]  (device-major) */
   const int32_t* edge_src;     /* [E] edge declaration order */
   const int32_t* edge_dst;     /* [E] */
-  const double* copy_ms;       /* [E][D][D]; diagonal ignored */
+  const double* copy_ms;       /* [E][D][D]; diagonal ignored; NaN = no link covers the copy (MissingLink
+                                  when build_model / an evaluator / a charged objective_value copy needs it) */
   const int64_t* budget_bytes; /* [D] */
   /* optional energy model (model.hpp:50-56); has_energy = 0 -> none */
   int32_t has_energy;

@@ -202,6 +202,18 @@ int xe_problem_create(const xe_problem_desc* d, int device, xe_problem** out) {
     h.src = vec(d->edge_src, static_cast<size_t>(h.E));
     h.dst = vec(d->edge_dst, static_cast<size_t>(h.E));
     h.w = vec(d->copy_ms, static_cast<size_t>(h.E) * h.D * h.D);
+    // NaN: no link covers the copy; raised when a model or a charged copy
+    // needs it (copy_cost, problem.cpp:374-376)
+    h.w_missing.assign(h.w.size(), 0);
+    for (size_t k = 0; k < h.w.size(); ++k)
+      if (std::isnan(h.w[k])) {
+        const int a = static_cast<int>(k / h.D % h.D), b = static_cast<int>(k % h.D);
+        if (a == b) fail(XE_ERR_ARG, "copy_ms must be finite on the diagonal");
+        if (h.missing_link.empty())
+          h.missing_link = "no link covers " + h.device_ids[static_cast<size_t>(a)] + "->" + h.device_ids[static_cast<size_t>(b)];
+        h.w_missing[k] = 1;
+        h.w[k] = 0.0;
+      }
     h.budget = vec(d->budget_bytes, static_cast<size_t>(h.D));
     for (int64_t m : h.mass)
       if (m <= 0) fail(XE_ERR_NON_POSITIVE_SIZE, "output_bytes must be positive");

@@ -220,8 +220,24 @@ void complete_cube_host(const xe_problem* pr, const xe_model_opts& o, const uint
 
 double objective_dense_host(const xe_problem* pr, const xe_model_opts& o, const double* x_host) {
   const HostProblem& h = pr->h;
-  if (!h.missing_link.empty() && h.D > 1) fail(XE_ERR_MISSING_LINK, h.missing_link);
   const Cols C = cols_of(h);
+  // objective_value prices a copy only when it is charged, R(dc,t,dst) != 0
+  // and Z(ds,t,src) != 0, and copy_cost raises MissingLink there
+  // (model.cpp:399-411, problem.cpp:374-376): the same lazy check, in the
+  // reference's loop order so the first charged uncovered pair is named
+  if (!h.missing_link.empty() && h.D > 1 && !h.w_missing.empty()) {
+    for (int64_t t = 0; t < h.T; ++t)
+      for (int64_t e = 0; e < h.E; ++e)
+        for (int64_t dc = 0; dc < h.D; ++dc) {
+          if (x_host[C.r(dc, t, h.dst[static_cast<size_t>(e)])] == 0.0) continue;
+          for (int64_t ds = 0; ds < h.D; ++ds) {
+            if (ds == dc || x_host[C.z(ds, t, h.src[static_cast<size_t>(e)])] == 0.0) continue;
+            if (h.w_missing[static_cast<size_t>((e * h.D + ds) * h.D + dc)])
+              fail(XE_ERR_MISSING_LINK, "no link covers " + h.device_ids[static_cast<size_t>(ds)] + "->" +
+                                            h.device_ids[static_cast<size_t>(dc)]);
+          }
+        }
+  }
   cudaStream_t s = pr->stream;
   DevBuf<double> dx, dout;
   dx.alloc(static_cast<size_t>(C.n()));

@@ -205,7 +205,17 @@ Desc describe(const Problem& p, const std::optional<EnergyModel>& energy) {
     d.dst.push_back(edge.dst);
     for (int a = 0; a < d.D; ++a)
       for (int b = 0; b < d.D; ++b)
-        if (a != b) d.w[(static_cast<size_t>(e) * d.D + a) * d.D + b] = copy_cost(p, edge, a, b);
+        if (a != b) {
+          // an uncovered pair travels as NaN: the library raises MissingLink
+          // when a model or a charged copy needs it, as copy_cost does
+          double w = std::numeric_limits<double>::quiet_NaN();
+          try {
+            w = copy_cost(p, edge, a, b);
+          } catch (const Error& err) {
+            if (err.code() != Errc::MissingLink) throw;
+          }
+          d.w[(static_cast<size_t>(e) * d.D + a) * d.D + b] = w;
+        }
   }
   if (energy) {
     check_energy(*energy, d.D, d.T);

@@ -251,6 +251,7 @@ Doc read_training(const json& doc, bool chain) {
 void resolve_copies(Doc& doc) {
   HostProblem& p = doc.p;
   p.w.assign(static_cast<size_t>(p.E) * p.D * p.D, 0.0);
+  p.w_missing.assign(static_cast<size_t>(p.E) * p.D * p.D, 0);
   for (int e = 0; e < p.E; ++e)
     for (int a = 0; a < p.D; ++a)
       for (int b = 0; b < p.D; ++b) {
@@ -277,6 +278,7 @@ void resolve_copies(Doc& doc) {
             if (p.missing_link.empty())
               p.missing_link = "no link covers " + p.device_ids[static_cast<size_t>(a)] + "->" +
                                p.device_ids[static_cast<size_t>(b)];
+            p.w_missing[(static_cast<size_t>(e) * p.D + a) * p.D + b] = 1;
             continue;
           }
           v = best->latency + static_cast<double>(p.mass[static_cast<size_t>(p.src[static_cast<size_t>(e)])]) / best->rate;

@@ -105,6 +105,7 @@ struct HostProblem {
   std::vector<uint8_t> has_lim; // [D]
   std::vector<double> lim;      // [D]
   std::string missing_link;     // non-empty: some (edge, ds, dc) has no covering link
+  std::vector<uint8_t> w_missing;  // [E][D][D] 1 = no link covers the copy (w = 0 there)
 };
 
 HostProblem load_problem_json(const std::string& text);  // loader.cpp

@@ -568,6 +568,15 @@ void device_cases() {
     CHECK(action_cost(p, Action{ActionKind::Copy, 1, 0, -1, -1, 0, 1, 0, 1}) == 1.0);
     CHECK(action_cost(p, Action{ActionKind::Free, 1, 1, 1, -1, 0, 1, -1, -1}) == 0.0);
   });
+  run("objective_value raises MissingLink only for a charged uncovered copy (copy_cost is lazy)", [] {
+    Problem p = fixture("fig2");
+    const double full = objective_value(save_all_assignment(p, {0, 1, 1, 1, 1, 1, 1}), p);
+    Problem q = p;
+    q.edges[0].override_copy_ms.erase({1, 0});  // edge 0 -> 1 has no gpu -> cpu cost now
+    CHECK_THROWS_CODE(build_model(q), Errc::MissingLink);  // the model prices every copy
+    CHECK(objective_value(save_all_assignment(q, {0, 1, 1, 1, 1, 1, 1}), q) == full);
+    CHECK_THROWS_CODE(objective_value(save_all_assignment(q, {1, 0, 0, 0, 0, 0, 0}), q), Errc::MissingLink);
+  });
   run("solve_search: F1 chain3 = 9.0, proven by the LP bound", [] {
     Problem p = fixture("chain3");
     SearchParams sp;
