@@ -226,7 +226,8 @@ def placement_config(n, hbm):
             "gather_roofline": {"bound": "smem gather", "gathers_per_placement": gathers,
                                 "achieved": rate * gathers, "peak": lds_peak, "unit": "gathers/s",
                                 "frac": rate * gathers / lds_peak,
-                                "peak_note": "148 SMs x 32 banks x 1 access/clock at 1965 MHz"}}
+                                "peak_note": "148 SMs x 32 banks x 1 access/clock at 1965 MHz"},
+            "issue_roofline": issue_roofline("random2000", rate, None)}
 
 
 def reference_inrun(doc_vgg, doc_resnet):
