@@ -85,6 +85,7 @@ struct RoundArgs {
   int edits;
   double perturb;
   uint32_t* out;
+  int word_build;  // steps 1-2 word by word (long-lived tensors) instead of one atomic per saved bit
 };
 
 constexpr int kRoundWarps = 4;
@@ -93,10 +94,19 @@ constexpr int kRoundWarps = 4;
 // sequential walk over one cube; run by lane 0 of the candidate's warp
 // (round_kernel) or by one lane per candidate (round_batch_kernel) — the
 // same code, so both produce the same cubes.
+// fast: the cube was built here from a placement (no base): every timestep
+// tt computes op tt (its diagonal R bit), and the only other computations are
+// the recomputations this function adds, at the timesteps listed in rts — so
+// "the latest step in (u, hi) that computes a consumer of u" is the top
+// consumer bit of u below hi or one of those few steps, instead of a backward
+// scan over every timestep's rows.  Both give the same step.
 __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* dev, const uint32_t* cons,
-                               const int* last, const int* elig, int n_elig_v, uint64_t c) {
+                               const int* last, const int* elig, int n_elig_v, uint64_t c, bool fast) {
   const int D = a.D, T = a.T, W = a.W32;
   (void)last;
+  constexpr int kMaxRts = 16;
+  int rts[kMaxRts];
+  int nrts = 0;
   auto consumer_at = [&](int u, int tt) {
     uint32_t hit = 0u;
     for (int w = 0; w < W; ++w) {
@@ -114,6 +124,33 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
   };
   auto bit_get = [&](int which, int d, int t, int i) -> bool {
     return (cube[((which * D + d) * T + t) * W + (i >> 5)] >> (i & 31)) & 1u;
+  };
+  // latest tt in (u, hi) with consumer_at(u, tt), or u when there is none
+  auto last_consumer = [&](int u, int hi) -> int {
+    if (!fast) {
+      for (int tt = hi - 1; tt > u; --tt)
+        if (consumer_at(u, tt)) return tt;
+      return u;
+    }
+    int best = u;
+    for (int w = W - 1; w >= 0; --w) {
+      const int lo = 32 * w;
+      uint32_t m = cons[u * W + w];
+      // keep bits tt with u < tt < hi
+      if (hi <= lo) m = 0u;
+      else if (hi < lo + 32) m &= (1u << (hi - lo)) - 1u;
+      if (u + 1 >= lo + 32) m = 0u;
+      else if (u + 1 > lo) m &= ~0u << (u + 1 - lo);
+      if (m) {
+        best = lo + 31 - __clz(m);
+        break;
+      }
+    }
+    for (int k = 0; k < nrts; ++k) {
+      const int tt = rts[k];
+      if (tt > best && tt < hi && consumer_at(u, tt)) best = tt;
+    }
+    return best;
   };
   Philox rng(a.seed, c, 0x1u);
   for (int ed = 0; ed < a.edits; ++ed) {
@@ -162,13 +199,16 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
     }
     // the drop window must not cover a timestep where i is needed: any
     // earlier computation (diagonal or recomputed) of a consumer of i
-    int a0 = i + 1;
-    for (int tt = t - 1; tt > i; --tt)
-      if (consumer_at(i, tt)) {
-        a0 = tt + 1;
-        break;
-      }
+    const int a0 = last_consumer(i, t) + 1;
     if (a0 > t) continue;
+    if (fast) {  // t receives recomputations below
+      bool seen = false;
+      for (int k = 0; k < nrts; ++k) seen |= rts[k] == t;
+      if (!seen) {
+        if (nrts < kMaxRts) rts[nrts++] = t;
+        else fast = false;  // list full: back to the scan (same answers)
+      }
+    }
     // drop the whole window when the LP chose the spot, else a random tail of it
     const int a1 = lp_dev >= 0 ? a0 : a0 + rng.below(t - a0 + 1);
     int dn = lp_dev >= 0 ? lp_dev : (rng.uniform() < 0.5 ? rng.below(D) : dev[t]);
@@ -210,12 +250,7 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
         if (a.cost[dr * T + p] >= 1.0e9) dr = dvn;
         if (sp < 32 && a.cost[dr * T + p] < 1.0e9 && rng.uniform() < 0.5) {
           // first step after p's last use before t
-          int from = p + 1;
-          for (int tt = t - 1; tt > p; --tt)
-            if (consumer_at(p, tt)) {
-              from = tt + 1;
-              break;
-            }
+          const int from = last_consumer(p, t) + 1;
           recompute_at(p, from, dr);
           stack[sp] = p;
           sdev[sp++] = dr;
@@ -238,6 +273,59 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
 }
 
 
+// alive[t][w]: ops i of word w with i < t <= last[i] (the minimal-save set
+// of timestep t, candidate-independent); block-cooperative
+__device__ void build_alive(uint32_t* alive, const int* last, int T, int W) {
+  for (int q = threadIdx.x; q < T * W; q += blockDim.x) {
+    const int t = q / W, w = q % W;
+    uint32_t m = 0u;
+    for (int b = 0; b < 32; ++b) {
+      const int i = 32 * w + b;
+      if (i < T && i < t && t <= last[i]) m |= 1u << b;
+    }
+    alive[q] = m;
+  }
+}
+
+// Steps 1-2 written word by word by one warp: R(d,t) = {t} when dev_t = d,
+// S(d,t) = alive(t) & the ops placed on d (dm: per-warp [D][W] scratch)
+__device__ void build_minimal_save(uint32_t* cube, const int* dev, const uint32_t* alive, uint32_t* dm, int D, int T,
+                                   int W, int lane) {
+  for (int w = 0; w < W; ++w) {
+    const int i = 32 * w + lane;
+    const int di = i < T ? dev[i] : -1;
+    for (int d = 0; d < D; ++d) {
+      const unsigned m = __ballot_sync(0xffffffffu, di == d);
+      if (lane == 0) dm[d * W + w] = m;
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < T; t += 32) {
+    const int dt = dev[t];
+    for (int dd = 0; dd < D; ++dd)
+      for (int w = 0; w < W; ++w)
+        cube[(dd * T + t) * W + w] = (dt == dd && (t >> 5) == w) ? (1u << (t & 31)) : 0u;
+    for (int d = 0; d < D; ++d)
+      for (int w = 0; w < W; ++w) cube[((D + d) * T + t) * W + w] = alive[t * W + w] & dm[d * W + w];
+  }
+  __syncwarp();
+}
+
+// Steps 1-2 bit by bit (cheaper when tensors live briefly: one shared
+// atomic per saved bit instead of every word of the cube)
+__device__ void build_minimal_save_bits(uint32_t* cube, const int* dev, const int* last, int D, int T, int W,
+                                        int lane) {
+  const int words = 2 * D * T * W;
+  for (int i = lane; i < words; i += 32) cube[i] = 0u;
+  __syncwarp();
+  for (int i = lane; i < T; i += 32) {
+    const int d = dev[i];
+    atomicOr(&cube[(d * T + i) * W + (i >> 5)], 1u << (i & 31));
+    for (int t = i + 1; t <= last[i]; ++t) atomicOr(&cube[((D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -248,8 +336,10 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   int* last = reinterpret_cast<int*>(cons + T * W);
   int* elig = last + T;      // ops with a consumer beyond i+1, ascending
   int* n_elig = elig + T;
-  uint32_t* cube = reinterpret_cast<uint32_t*>(n_elig + 1) + wid * (words + T);
+  uint32_t* alive = reinterpret_cast<uint32_t*>(n_elig + 1);  // [T][W]
+  uint32_t* cube = alive + T * W + wid * (words + T);
   int* dev = reinterpret_cast<int*>(cube + words);
+  uint32_t* dm = alive + T * W + kRoundWarps * (words + T) + wid * D * W;  // [D][W]
   for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
   for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
   __syncthreads();
@@ -264,10 +354,8 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       if (last[j] > j + 1) elig[ne++] = j;
     *n_elig = ne;
   }
+  build_alive(alive, last, T, W);
   __syncthreads();
-  auto bit_set = [&](int which, int d, int t, int i) {
-    atomicOr(&cube[((which * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
-  };
   // plain read-modify-write for the single-lane sections (lane 0 edits)
   auto bset = [&](int which, int d, int t, int i) {
     cube[((which * D + d) * T + t) * W + (i >> 5)] |= 1u << (i & 31);
@@ -282,7 +370,8 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * kRoundWarps + wid; k < a.n;
        k += static_cast<int64_t>(gridDim.x) * kRoundWarps) {
     const uint64_t c = static_cast<uint64_t>(a.first + k);
-    for (int i = lane; i < words; i += 32) cube[i] = a.base ? a.base[i] : 0u;
+    if (a.base)
+      for (int i = lane; i < words; i += 32) cube[i] = a.base[i];
     __syncwarp();
     if (a.base) {
       // local search around a base schedule: devices from its diagonal, then
@@ -343,13 +432,12 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
     }
     __syncwarp();
     // 2. diagonal + minimal-save
-    for (int i = lane; i < T && !a.base; i += 32) {
-      bit_set(0, dev[i], i, i);
-      for (int t = i + 1; t <= last[i]; ++t) bit_set(1, dev[i], t, i);
+    if (!a.base) {
+      if (a.word_build) build_minimal_save(cube, dev, alive, dm, D, T, W, lane);
+      else build_minimal_save_bits(cube, dev, last, D, T, W, lane);
     }
-    __syncwarp();
     // 3-4. drop-and-recompute edits and perturbation (lane 0, sequential)
-    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c);
+    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c, a.base == nullptr);
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k) * words;
     for (int i = lane; i < words; i += 32) out[i] = cube[i];
@@ -373,7 +461,9 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
   int* last = reinterpret_cast<int*>(cons + T * W);
   int* elig = last + T;
   int* n_elig = elig + T;
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(n_elig + 1) + static_cast<size_t>(wid) * B * stride;
+  uint32_t* alive = reinterpret_cast<uint32_t*>(n_elig + 1);  // [T][W]: i < t <= last[i]
+  uint32_t* wbuf = alive + T * W + static_cast<size_t>(wid) * B * stride;
+  uint32_t* dm = alive + T * W + static_cast<size_t>(warps) * B * stride + wid * D * W;  // [D][W] ops per device
   for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
   for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
   __syncthreads();
@@ -388,6 +478,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
       if (last[j] > j + 1) elig[ne++] = j;
     *n_elig = ne;
   }
+  build_alive(alive, last, T, W);
   __syncthreads();
   const int n_el = *n_elig;
   for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * warps + wid) * B; k0 < a.n;
@@ -397,7 +488,6 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
       const uint64_t c = static_cast<uint64_t>(a.first + k0 + j);
       uint32_t* cube = wbuf + static_cast<size_t>(j) * stride;
       int* dev = reinterpret_cast<int*>(cube + words);
-      for (int i = lane; i < words; i += 32) cube[i] = 0u;
       // 1. placement, one Philox stream per (candidate, op)
       for (int i = lane; i < T; i += 32) {
         Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
@@ -426,19 +516,15 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
         dev[i] = pick;
       }
       __syncwarp();
-      // 2. diagonal + minimal-save
-      for (int i = lane; i < T; i += 32) {
-        const int d = dev[i];
-        atomicOr(&cube[((0 * D + d) * T + i) * W + (i >> 5)], 1u << (i & 31));
-        for (int t = i + 1; t <= last[i]; ++t) atomicOr(&cube[((1 * D + d) * T + t) * W + (i >> 5)], 1u << (i & 31));
-      }
-      __syncwarp();
+      // 2. diagonal + minimal-save, word by word (measured faster here at
+      // every cube size the batched kernel takes)
+      build_minimal_save(cube, dev, alive, dm, D, T, W, lane);
     }
     // 3-4. one lane per candidate
     if (lane < nb) {
       uint32_t* cube = wbuf + static_cast<size_t>(lane) * stride;
       edit_candidate(a, cube, reinterpret_cast<const int*>(cube + words), cons, last, elig, n_el,
-                     static_cast<uint64_t>(a.first + k0 + lane));
+                     static_cast<uint64_t>(a.first + k0 + lane), true);
     }
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k0) * words;
@@ -803,14 +889,24 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.perturb = perturb;
   a.out = out;
   const int words = 2 * h.D * h.T * a.W32;
-  const int smem = (h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T)) * 4;
+  {  // word-by-word steps 1-2 when the saved bits outnumber the cube's words
+    int64_t saves = 0;
+    std::vector<int> lastc(static_cast<size_t>(h.T), -1);
+    for (int e = 0; e < h.E; ++e)
+      lastc[static_cast<size_t>(h.src[static_cast<size_t>(e)])] =
+          std::max(lastc[static_cast<size_t>(h.src[static_cast<size_t>(e)])], h.dst[static_cast<size_t>(e)]);
+    for (int i = 0; i < h.T; ++i) saves += std::max(0, lastc[static_cast<size_t>(i)] - i);
+    a.word_build = saves > words ? 1 : 0;
+    if (const char* e = std::getenv("XE_ROUND_WORD")) a.word_build = e[0] == '1';
+  }
+  const int smem = (2 * h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T + h.D * a.W32)) * 4;
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
   {  // lane per candidate when 32 cubes per warp fit (base cubes keep round_kernel)
-    const int tables = (h.T * a.W32 + 2 * h.T + 1) * 4;
+    const int tables = (2 * h.T * a.W32 + 2 * h.T + 1) * 4;  // cons, last, elig, n_elig, alive
     const char* e = std::getenv("XE_ROUND_BATCH");
-    const int B = e ? std::max(0, std::min(32, std::atoi(e))) : 8;  // candidates per warp (0: round_kernel); 8 measured best
-    const int per_warp = B * (words + h.T) * 4;
+    const int B = e ? std::max(0, std::min(32, std::atoi(e))) : 6;  // candidates per warp (0: round_kernel); 6 measured best
+    const int per_warp = B * (words + h.T) * 4 + h.D * a.W32 * 4;
     const int warps = B > 0 ? std::min(8, (limit - tables) / std::max(1, per_warp)) : 0;
     // below 4 warps per CTA (large cubes: ResNet-50 holds one) the warp per
     // candidate kernel keeps more candidates in flight
