@@ -43,6 +43,7 @@ struct Args {
   const double* w;        // [E][D][D]
   const int64_t* tfix;    // [D*T + E*D*D] fixed point
   const int64_t* tfix_edge;  // [E] when every cross-device copy of an edge costs the same (else null)
+  const int64_t* tfix_op;    // [T][D] fixed-point compute costs, op-major (sliced kernel)
   const int32_t* src;
   const int32_t* dst;
   const int32_t* eorder;  // edges sorted by (dst, e)
@@ -282,18 +283,25 @@ __global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args 
         }
       }
       const int jn = min(16, T - 16 * b);  // warp-uniform
+      const int64_t* tf = a.tfix_op + static_cast<int64_t>(16 * b) * D;
+      const int64_t* ms = a.mass + 16 * b;
+      // op j of the block: bit b of its device byte by an immediate mask
+      auto op = [&](int j) {
+        const uint32_t x = wv[j >> 2];
+        const int sh = 8 * (j & 3);
+        const int d = static_cast<int>((x >> sh) & 0xffu);
+        const unsigned p0 = __ballot_sync(0xffffffffu, x & (1u << sh));
+        const unsigned p1 = NB > 1 ? __ballot_sync(0xffffffffu, x & (2u << sh)) : 0u;
+        const unsigned p2 = NB > 2 ? __ballot_sync(0xffffffffu, x & (4u << sh)) : 0u;
+        if (lane == 0) planes[16 * b + j] = make_uint4(p0, p1, p2, 0u);
+        fix += __ldg(tf + j * D + d);
+        s_acc[(wid * 8 + d) * 32 + lane] += __ldg(ms + j);
+      };
+      if (jn == 16) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < jn) {
-          const int i = 16 * b + j;
-          const int d = static_cast<int>((wv[j >> 2] >> (8 * (j & 3))) & 0xffu);
-          const unsigned p0 = __ballot_sync(0xffffffffu, d & 1);
-          const unsigned p1 = NB > 1 ? __ballot_sync(0xffffffffu, (d >> 1) & 1) : 0u;
-          const unsigned p2 = NB > 2 ? __ballot_sync(0xffffffffu, (d >> 2) & 1) : 0u;
-          if (lane == 0) planes[i] = make_uint4(p0, p1, p2, 0u);
-          fix += __ldg(a.tfix + d * T + i);
-          s_acc[(wid * 8 + d) * 32 + lane] += __ldg(a.mass + i);
-        }
+        for (int j = 0; j < 16; ++j) op(j);
+      } else {
+        for (int j = 0; j < jn; ++j) op(j);
       }
     }
     __syncthreads();
@@ -366,6 +374,12 @@ __global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args 
       a.wvalid[blockIdx.x] = nv;
     }
   }
+}
+
+// op-major copy of the [D][T] fixed-point compute costs
+__global__ void transpose_fix_kernel(const int64_t* tfix, int D, int T, int64_t* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < D * T) out[(k % T) * D + k / T] = tfix[k];
 }
 
 // ---- assignment oracle: thread per odometer index -------------------------
@@ -532,6 +546,11 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
     int dev_smem = 0;
     XE_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
     if (smem_sl <= static_cast<size_t>(dev_smem)) {
+      DevBuf<int64_t> top;
+      top.alloc(static_cast<size_t>(h.T) * h.D);
+      place::transpose_fix_kernel<<<std::max(1, (h.T * h.D + 255) / 256), 256, 0, s>>>(a.tfix, h.D, h.T, top.p);
+      XE_CUDA(cudaGetLastError());
+      a.tfix_op = top.p;
       auto ks = h.D <= 2 ? place::place_sliced_kernel<1> : h.D <= 4 ? place::place_sliced_kernel<2>
                                                                      : place::place_sliced_kernel<3>;
       XE_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_sl)));
