@@ -258,50 +258,57 @@ __global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args 
     int64_t fix = 0;
 #pragma unroll
     for (int x = 0; x < 8; ++x) s_acc[(wid * 8 + x) * 32 + lane] = 0;
-    // ---- phase 1: ops
-    uint4 vnext = (vec && live && wid < nblk) ? __ldg(reinterpret_cast<const uint4*>(row) + wid) : make_uint4(0, 0, 0, 0);
-    for (int b = wid; b < nblk; b += kSlWarps) {
-      uint32_t wv[4];
-      if (vec) {
-        // the next block's bytes are in flight while this block is processed
-        const uint4 v = vnext;
-        if (live && b + kSlWarps < nblk) vnext = __ldg(reinterpret_cast<const uint4*>(row) + b + kSlWarps);
-        wv[0] = v.x;
-        wv[1] = v.y;
-        wv[2] = v.z;
-        wv[3] = v.w;
-      } else {
+    // ---- phase 1: ops, kG blocks of 16 per warp at a time: their bytes are
+    // loaded together, then consumed (the loads of a group overlap)
+    constexpr int kG = 4;
+    for (int b0 = wid; b0 < nblk; b0 += kG * kSlWarps) {
+      uint4 vg[kG];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t x = 0;
+      for (int g = 0; g < kG; ++g) {
+        const int b = b0 + g * kSlWarps;
+        if (vec) {
+          vg[g] = (live && b < nblk) ? __ldg(reinterpret_cast<const uint4*>(row) + b) : make_uint4(0, 0, 0, 0);
+        } else {
+          uint32_t w4[4];
 #pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            const int i = 16 * b + 4 * q + y;
-            if (live && i < T) x |= static_cast<uint32_t>(row[i]) << (8 * y);
+          for (int q = 0; q < 4; ++q) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              const int i = 16 * b + 4 * q + y;
+              if (live && b < nblk && i < T) x |= static_cast<uint32_t>(row[i]) << (8 * y);
+            }
+            w4[q] = x;
           }
-          wv[q] = x;
+          vg[g] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
       }
-      const int jn = min(16, T - 16 * b);  // warp-uniform
-      const int64_t* tf = a.tfix_op + static_cast<int64_t>(16 * b) * D;
-      const int64_t* ms = a.mass + 16 * b;
-      // op j of the block: bit b of its device byte by an immediate mask
-      auto op = [&](int j) {
-        const uint32_t x = wv[j >> 2];
-        const int sh = 8 * (j & 3);
-        const int d = static_cast<int>((x >> sh) & 0xffu);
-        const unsigned p0 = __ballot_sync(0xffffffffu, x & (1u << sh));
-        const unsigned p1 = NB > 1 ? __ballot_sync(0xffffffffu, x & (2u << sh)) : 0u;
-        const unsigned p2 = NB > 2 ? __ballot_sync(0xffffffffu, x & (4u << sh)) : 0u;
-        if (lane == 0) planes[16 * b + j] = make_uint4(p0, p1, p2, 0u);
-        fix += __ldg(tf + j * D + d);
-        s_acc[(wid * 8 + d) * 32 + lane] += __ldg(ms + j);
-      };
-      if (jn == 16) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) op(j);
-      } else {
-        for (int j = 0; j < jn; ++j) op(j);
+      for (int g = 0; g < kG; ++g) {
+        const int b = b0 + g * kSlWarps;
+        if (b >= nblk) break;  // warp-uniform
+        const uint32_t wv[4] = {vg[g].x, vg[g].y, vg[g].z, vg[g].w};
+        const int jn = min(16, T - 16 * b);  // warp-uniform
+        const int64_t* tf = a.tfix_op + static_cast<int64_t>(16 * b) * D;
+        const int64_t* ms = a.mass + 16 * b;
+        // op j of the block: bit b of its device byte by an immediate mask
+        auto op = [&](int j) {
+          const uint32_t x = wv[j >> 2];
+          const int sh = 8 * (j & 3);
+          const int d = static_cast<int>((x >> sh) & 0xffu);
+          const unsigned p0 = __ballot_sync(0xffffffffu, x & (1u << sh));
+          const unsigned p1 = NB > 1 ? __ballot_sync(0xffffffffu, x & (2u << sh)) : 0u;
+          const unsigned p2 = NB > 2 ? __ballot_sync(0xffffffffu, x & (4u << sh)) : 0u;
+          if (lane == 0) planes[16 * b + j] = make_uint4(p0, p1, p2, 0u);
+          fix += __ldg(tf + j * D + d);
+          s_acc[(wid * 8 + d) * 32 + lane] += __ldg(ms + j);
+        };
+        if (jn == 16) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) op(j);
+        } else {
+          for (int j = 0; j < jn; ++j) op(j);
+        }
       }
     }
     __syncthreads();
