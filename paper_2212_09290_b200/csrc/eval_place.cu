@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kWarps * 32) place_kernel(const Args a) {
 constexpr int kSlWarps = XE_SL_WARPS;
 
 template <int NB>
-__global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args a) {
+__global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args a, int acc32) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int T = a.T, D = a.D, E = a.E;
@@ -313,17 +313,24 @@ __global__ void __launch_bounds__(kSlWarps * 32) place_sliced_kernel(const Args 
     }
     __syncthreads();
     // ---- phase 2: edges
+    // a warp's edge costs sum in 32 bits when they cannot overflow
+    // (acc32, checked on the host), else in 64
+    auto edges = [&](auto acc) {
 #pragma unroll 4
-    for (int e = e0; e < e1; ++e) {
-      const uint2 ed = s_edge[e];
-      const uint32_t sd = ed.x;
-      const uint4 pu = *reinterpret_cast<const uint4*>(pbase + (sd & 0xffffu));
-      const uint4 pv = *reinterpret_cast<const uint4*>(pbase + (sd >> 16));
-      unsigned diff = pu.x ^ pv.x;
-      if (NB > 1) diff |= pu.y ^ pv.y;
-      if (NB > 2) diff |= pu.z ^ pv.z;
-      if ((diff >> lane) & 1u) fix += static_cast<int32_t>(ed.y);
-    }
+      for (int e = e0; e < e1; ++e) {
+        const uint2 ed = s_edge[e];
+        const uint32_t sd = ed.x;
+        const uint4 pu = *reinterpret_cast<const uint4*>(pbase + (sd & 0xffffu));
+        const uint4 pv = *reinterpret_cast<const uint4*>(pbase + (sd >> 16));
+        unsigned diff = pu.x ^ pv.x;
+        if (NB > 1) diff |= pu.y ^ pv.y;
+        if (NB > 2) diff |= pu.z ^ pv.z;
+        if ((diff >> lane) & 1u) acc += static_cast<decltype(acc)>(ed.y);
+      }
+      return acc;
+    };
+    if (acc32) fix += static_cast<int64_t>(edges(0u));
+    else fix += edges(int64_t(0));
     s_fix[wid * 32 + lane] = fix;
     __syncthreads();
     // ---- warp 0: totals, flags, outputs
@@ -504,6 +511,7 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
   // config-5 generator): the compact per-edge table
   DevBuf<int64_t> tedge;
   bool tedge32 = false;
+  int64_t tedge_max = 0;
   if (pr->fix_k_place >= 0 && h.D > 1) {
     bool uniform = true;
     std::vector<int64_t> te(static_cast<size_t>(h.E));
@@ -521,6 +529,7 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
       tedge.upload(te, s);
       a.tfix_edge = tedge.p;
       tedge32 = std::all_of(te.begin(), te.end(), [](int64_t v) { return v >= INT32_MIN && v <= INT32_MAX; });
+      for (int64_t v : te) tedge_max = std::max(tedge_max, v);
     }
   }
   a.src = pr->d_src.p;
@@ -568,7 +577,11 @@ void eval_placements_device(const xe_problem* pr, const uint8_t* dev, int64_t n,
       const int grid = static_cast<int>(std::max<int64_t>(
           1, std::min<int64_t>(groups, static_cast<int64_t>(nsm) * std::max(1, std::min(per_sm, 8)))));
       if (n > 0) {
-        ks<<<grid, place::kSlWarps * 32, smem_sl, s>>>(a);
+        // 32-bit edge sums when a warp's share of the edges cannot overflow them
+        const int64_t cmax = tedge_max;
+        const int64_t per_warp = (h.E + place::kSlWarps - 1) / place::kSlWarps;
+        const int acc32 = cmax * per_warp < (int64_t(1) << 32) ? 1 : 0;
+        ks<<<grid, place::kSlWarps * 32, smem_sl, s>>>(a, acc32);
         XE_CUDA(cudaGetLastError());
       }
       if (best3) {
