@@ -2,8 +2,8 @@
 """One small invocation of every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck):  K1 build + CSC, K3 PDHG (a few hundred
 iterations), K4 rounding + moves + placements, K2a streaming + reference-order
-evaluators (fig2, VGG-16, ResNet-50 shapes), K2b placements + oracle, the
-search, solve_exact, schedule decode / validate / replay."""
+evaluators (fig2, VGG-16, ResNet-50 shapes), K2b placements (both kernels) + oracle,
+the search, solve_exact, schedule decode / validate / replay, device MPS."""
 import os
 import sys
 
@@ -21,6 +21,7 @@ fig2 = open(os.path.join(ROOT, "tests", "golden", "problems", "fig2.json")).read
 for name, doc, n in (("fig2", fig2, 300), ("vgg16", configs.vgg16_doc(), 2048), ("resnet50", configs.resnet50_doc(), 256)):
     p = xe.Problem.from_json(doc)
     m = xe.build_model(p)
+    m.write_mps()                                         # device MPS emission
     m.csc()
     xe.pdhg_solve(m, tol=1e-3, max_iters=256)
     cubes = xe.round_cubes(p, n, 7, edits=3, perturb=0.1)
@@ -42,6 +43,9 @@ for name, doc, n in (("fig2", fig2, 300), ("vgg16", configs.vgg16_doc(), 2048), 
         if good:
             sch.replay(p, good)
     print(name, "ok", r.best_obj, flush=True)
+p5 = xe.Problem.from_json(configs.random2000_doc())
+xe.evaluate_placements(p5, xe.random_placements(p5, 96, 3), policy=0)  # bit-sliced K2b (D = 8)
+print("random2000 ok", flush=True)
 p = xe.Problem.from_json(fig2)
 xe.assignment_oracle(p)
 print("exact", xe.solve_exact(p).objective)
