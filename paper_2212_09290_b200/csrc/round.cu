@@ -86,6 +86,7 @@ struct RoundArgs {
   double perturb;
   uint32_t* out;
   int word_build;  // steps 1-2 word by word (long-lived tensors) instead of one atomic per saved bit
+  int slow_scan;   // XE_ROUND_SLOW_SCAN=1: the edits' backward row scans (test of the fast lookup)
 };
 
 constexpr int kRoundWarps = 4;
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       else build_minimal_save_bits(cube, dev, last, D, T, W, lane);
     }
     // 3-4. drop-and-recompute edits and perturbation (lane 0, sequential)
-    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c, a.base == nullptr);
+    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c, a.base == nullptr && !a.slow_scan);
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k) * words;
     for (int i = lane; i < words; i += 32) out[i] = cube[i];
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
     if (lane < nb) {
       uint32_t* cube = wbuf + static_cast<size_t>(lane) * stride;
       edit_candidate(a, cube, reinterpret_cast<const int*>(cube + words), cons, last, elig, n_el,
-                     static_cast<uint64_t>(a.first + k0 + lane), true);
+                     static_cast<uint64_t>(a.first + k0 + lane), !a.slow_scan);
     }
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k0) * words;
@@ -898,6 +899,8 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     for (int i = 0; i < h.T; ++i) saves += std::max(0, lastc[static_cast<size_t>(i)] - i);
     a.word_build = saves > words ? 1 : 0;
     if (const char* e = std::getenv("XE_ROUND_WORD")) a.word_build = e[0] == '1';
+    const char* sc = std::getenv("XE_ROUND_SLOW_SCAN");
+    a.slow_scan = sc && sc[0] == '1';
   }
   const int smem = (2 * h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T + h.D * a.W32)) * 4;
   int limit = 0;

@@ -124,3 +124,18 @@ def test_large_lp(name):
         assert abs(r.primal_obj - want) <= 1e-5 * abs(want), (r.primal_obj, want, r.iters)
         assert lower <= want + 1e-9 * abs(want)
     print(f"{name}: LP in [{lower!r}, {upper!r}] (PDHG {r.primal_obj!r}, {r.iters} iterations)")
+
+
+def test_coded_entries_match_fp64_entries(monkeypatch):
+    # config 3's model (4.3 M entries, 15 distinct values): the coded half-steps
+    # (index | code << 24, scaling on the vectors) and the scaled fp64 entries
+    # solve the same LP to the same certified optimum
+    m = xe.build_model(problem("resnet50"))
+    coded = xe.pdhg_solve(m, tol=1e-7, max_iters=1000000, return_x=True, return_y=True)
+    monkeypatch.setenv("XE_PDHG_CODED", "0")
+    plain = xe.pdhg_solve(m, tol=1e-7, max_iters=1000000)
+    assert coded.coded and not plain.coded
+    assert coded.converged and plain.converged and coded.certified
+    assert abs(coded.primal_obj - plain.primal_obj) <= 1e-7 * abs(plain.primal_obj)
+    assert abs(coded.dual_obj - plain.dual_obj) <= 1e-7 * abs(plain.dual_obj)
+    assert_certified(m, coded)

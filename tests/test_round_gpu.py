@@ -186,3 +186,25 @@ def test_batched_rounding_equals_warp_rounding(name):
     finally:
         del os.environ["XE_ROUND_BATCH"]
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name,edits", [("fig2", 6), ("vgg16", 4), ("resnet50", 5)])
+@pytest.mark.parametrize("batch", ["6", "0"])
+def test_fast_consumer_lookup_equals_row_scan(name, edits, batch, monkeypatch):
+    # the edits' "latest step before t computing a consumer of u" from the
+    # consumer rows + the candidate's own recomputation steps (default) and
+    # from the backward scan over every step's R rows (XE_ROUND_SLOW_SCAN=1),
+    # in both rounding kernels; and both minimal-save builds (word by word /
+    # one atomic per saved bit, XE_ROUND_WORD) give the same cubes
+    text = golden_problem_text(name) if name == "fig2" else configs.CONFIGS[name]()
+    prob = xe.Problem.from_json(text)
+    monkeypatch.setenv("XE_ROUND_BATCH", batch)
+    n = 2000 if name != "resnet50" else 300
+    a = xe.round_cubes(prob, n, seed=5, first=3, edits=edits, perturb=0.1)
+    monkeypatch.setenv("XE_ROUND_SLOW_SCAN", "1")
+    b = xe.round_cubes(prob, n, seed=5, first=3, edits=edits, perturb=0.1)
+    assert torch.equal(a, b)
+    monkeypatch.delenv("XE_ROUND_SLOW_SCAN")
+    for w in ("0", "1"):
+        monkeypatch.setenv("XE_ROUND_WORD", w)
+        assert torch.equal(xe.round_cubes(prob, n, seed=5, first=3, edits=edits, perturb=0.1), a)
