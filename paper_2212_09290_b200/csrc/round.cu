@@ -92,19 +92,30 @@ struct RoundArgs {
 constexpr int kRoundWarps = 4;
 
 // Steps 3-4 of one candidate (drop-and-recompute edits, perturbation): a
-// sequential walk over one cube; run by lane 0 of the candidate's warp
-// (round_kernel) or by one lane per candidate (round_batch_kernel) — the
-// same code, so both produce the same cubes.
+// walk over one cube; run by the candidate's whole warp (round_kernel, the
+// timestep loops split across lanes) or by one lane per candidate
+// (round_batch_kernel) — the same code, so both produce the same cubes.
 // fast: the cube was built here from a placement (no base): every timestep
 // tt computes op tt (its diagonal R bit), and the only other computations are
 // the recomputations this function adds, at the timesteps listed in rts — so
 // "the latest step in (u, hi) that computes a consumer of u" is the top
 // consumer bit of u below hi or one of those few steps, instead of a backward
 // scan over every timestep's rows.  Both give the same step.
+// WARP: the whole warp runs one candidate's edits — every lane follows the
+// same (uniform) control flow and Philox draws, the loops over timesteps are
+// split across the lanes (each lane owns the rows of its timesteps, so no
+// two lanes write one word) and single-bit writes are lane 0's, with a warp
+// barrier before the next read.  Same cubes as the one-lane form.
+template <bool WARP>
 __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* dev, const uint32_t* cons,
                                const int* last, const int* elig, int n_elig_v, uint64_t c, bool fast) {
   const int D = a.D, T = a.T, W = a.W32;
   (void)last;
+  const int L0 = WARP ? static_cast<int>(threadIdx.x & 31) : 0;  // this lane's first offset
+  constexpr int LS = WARP ? 32 : 1;                               // loop stride
+  auto sync = [] {
+    if (WARP) __syncwarp();
+  };
   constexpr int kMaxRts = 16;
   int rts[kMaxRts];
   int nrts = 0;
@@ -129,9 +140,16 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
   // latest tt in (u, hi) with consumer_at(u, tt), or u when there is none
   auto last_consumer = [&](int u, int hi) -> int {
     if (!fast) {
-      for (int tt = hi - 1; tt > u; --tt)
-        if (consumer_at(u, tt)) return tt;
-      return u;
+      if constexpr (WARP) {
+        int best = u;
+        for (int tt = u + 1 + L0; tt < hi; tt += LS)
+          if (consumer_at(u, tt)) best = tt;
+        return static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(best)));
+      } else {
+        for (int tt = hi - 1; tt > u; --tt)
+          if (consumer_at(u, tt)) return tt;
+        return u;
+      }
     }
     int best = u;
     for (int w = W - 1; w >= 0; --w) {
@@ -218,14 +236,15 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
     // over [from, t]; later saves follow it to dr (EQ11 needs a holder at t)
     auto recompute_at = [&](int v, int from, int dr) {
       const int dv = dev[v];
-      for (int tt = from; tt <= t; ++tt) bclr(1, dv, tt, v);
-      bset(0, dr, t, v);
+      for (int tt = from + L0; tt <= t; tt += LS) bclr(1, dv, tt, v);
+      if (L0 == 0) bset(0, dr, t, v);
       if (dr != dv)
-        for (int tt = t + 1; tt < T; ++tt)
+        for (int tt = t + 1 + L0; tt < T; tt += LS)
           if (bit_get(1, dv, tt, v)) {
             bclr(1, dv, tt, v);
             bset(1, dr, tt, v);
           }
+      sync();
     };
     recompute_at(i, a1, dn);
     // parents of every op recomputed at t: keep them saved until t, or
@@ -259,17 +278,20 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
         }
         const int dp = dev[p];
         int ls = p;
-        for (int tt = p + 1; tt <= t; ++tt)
+        for (int tt = p + 1 + L0; tt <= t; tt += LS)
           if (bit_get(1, dp, tt, p)) ls = tt;
-        for (int tt = ls + 1; tt <= t; ++tt) bset(1, dp, tt, p);
+        if (WARP) ls = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(ls)));
+        for (int tt = ls + 1 + L0; tt <= t; tt += LS) bset(1, dp, tt, p);
+        sync();
       }
     }
   }
   // 4. perturbation
   if (rng.uniform() < a.perturb) {
     const int which = rng.below(2), d = rng.below(D), t = rng.below(T), i = rng.below(T);
-    cube[((which * D + d) * T + t) * W + (i >> 5)] ^= 1u << (i & 31);
+    if (L0 == 0) cube[((which * D + d) * T + t) * W + (i >> 5)] ^= 1u << (i & 31);
   }
+  sync();
 
 }
 
@@ -438,7 +460,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       else build_minimal_save_bits(cube, dev, last, D, T, W, lane);
     }
     // 3-4. drop-and-recompute edits and perturbation (lane 0, sequential)
-    if (lane == 0) edit_candidate(a, cube, dev, cons, last, elig, *n_elig, c, a.base == nullptr && !a.slow_scan);
+    edit_candidate<true>(a, cube, dev, cons, last, elig, *n_elig, c, a.base == nullptr && !a.slow_scan);
     __syncwarp();
     uint32_t* out = a.out + static_cast<size_t>(k) * words;
     for (int i = lane; i < words; i += 32) out[i] = cube[i];
@@ -524,7 +546,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
     // 3-4. one lane per candidate
     if (lane < nb) {
       uint32_t* cube = wbuf + static_cast<size_t>(lane) * stride;
-      edit_candidate(a, cube, reinterpret_cast<const int*>(cube + words), cons, last, elig, n_el,
+      edit_candidate<false>(a, cube, reinterpret_cast<const int*>(cube + words), cons, last, elig, n_el,
                      static_cast<uint64_t>(a.first + k0 + lane), !a.slow_scan);
     }
     __syncwarp();
