@@ -443,6 +443,8 @@ class Model:
         check(LIB.xe_write_mps(self._h, None, C.byref(n)))
         # the text is downloaded straight into a fresh, not yet shared bytes
         # object (one host pass instead of buffer + copy)
+        if n.value == 0:  # (the empty bytes object is shared: never written into)
+            return b""
         out = _new_bytes(None, n.value)
         check(LIB.xe_write_mps(self._h, C.c_char_p(out), C.byref(n)))
         return out
