@@ -298,9 +298,10 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
 
 // alive[t][w]: ops i of word w with i < t <= last[i] (the minimal-save set
 // of timestep t, candidate-independent); block-cooperative
-__device__ void build_alive(uint32_t* alive, const int* last, int T, int W) {
+__device__ void build_alive(uint32_t* alive, uint16_t* tq, const int* last, int T, int W) {
   for (int q = threadIdx.x; q < T * W; q += blockDim.x) {
     const int t = q / W, w = q % W;
+    tq[q] = static_cast<uint16_t>(t);
     uint32_t m = 0u;
     for (int b = 0; b < 32; ++b) {
       const int i = 32 * w + b;
@@ -312,8 +313,8 @@ __device__ void build_alive(uint32_t* alive, const int* last, int T, int W) {
 
 // Steps 1-2 written word by word by one warp: R(d,t) = {t} when dev_t = d,
 // S(d,t) = alive(t) & the ops placed on d (dm: per-warp [D][W] scratch)
-__device__ void build_minimal_save(uint32_t* cube, const int* dev, const uint32_t* alive, uint32_t* dm, int D, int T,
-                                   int W, int lane) {
+__device__ void build_minimal_save(uint32_t* cube, const int* dev, const uint32_t* alive, const uint16_t* tq,
+                                   uint32_t* dm, int D, int T, int W, int lane) {
   for (int w = 0; w < W; ++w) {
     const int i = 32 * w + lane;
     const int di = i < T ? dev[i] : -1;
@@ -323,13 +324,18 @@ __device__ void build_minimal_save(uint32_t* cube, const int* dev, const uint32_
     }
   }
   __syncwarp();
-  for (int t = lane; t < T; t += 32) {
+  // lanes over the words q = t*W + w of a (which, d) plane: consecutive
+  // lanes store consecutive words
+  const int TW = T * W;
+  for (int q = lane; q < TW; q += 32) {
+    const int t = tq[q], w = q - t * W;
     const int dt = dev[t];
-    for (int dd = 0; dd < D; ++dd)
-      for (int w = 0; w < W; ++w)
-        cube[(dd * T + t) * W + w] = (dt == dd && (t >> 5) == w) ? (1u << (t & 31)) : 0u;
-    for (int d = 0; d < D; ++d)
-      for (int w = 0; w < W; ++w) cube[((D + d) * T + t) * W + w] = alive[t * W + w] & dm[d * W + w];
+    const uint32_t bit = (t >> 5) == w ? (1u << (t & 31)) : 0u;
+    const uint32_t al = alive[q];
+    for (int d = 0; d < D; ++d) {
+      cube[d * TW + q] = dt == d ? bit : 0u;
+      cube[(D + d) * TW + q] = al & dm[d * W + w];
+    }
   }
   __syncwarp();
 }
@@ -360,9 +366,10 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
   int* elig = last + T;      // ops with a consumer beyond i+1, ascending
   int* n_elig = elig + T;
   uint32_t* alive = reinterpret_cast<uint32_t*>(n_elig + 1);  // [T][W]
-  uint32_t* cube = alive + T * W + wid * (words + T);
+  uint16_t* tq = reinterpret_cast<uint16_t*>(alive + T * W);     // [T*W]: t of word q
+  uint32_t* cube = alive + T * W + (T * W + 1) / 2 + wid * (words + T);
   int* dev = reinterpret_cast<int*>(cube + words);
-  uint32_t* dm = alive + T * W + kRoundWarps * (words + T) + wid * D * W;  // [D][W]
+  uint32_t* dm = alive + T * W + (T * W + 1) / 2 + kRoundWarps * (words + T) + wid * D * W;  // [D][W]
   for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
   for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
   __syncthreads();
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
       if (last[j] > j + 1) elig[ne++] = j;
     *n_elig = ne;
   }
-  build_alive(alive, last, T, W);
+  build_alive(alive, tq, last, T, W);
   __syncthreads();
   // plain read-modify-write for the single-lane sections (lane 0 edits)
   auto bset = [&](int which, int d, int t, int i) {
@@ -456,7 +463,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
     __syncwarp();
     // 2. diagonal + minimal-save
     if (!a.base) {
-      if (a.word_build) build_minimal_save(cube, dev, alive, dm, D, T, W, lane);
+      if (a.word_build) build_minimal_save(cube, dev, alive, tq, dm, D, T, W, lane);
       else build_minimal_save_bits(cube, dev, last, D, T, W, lane);
     }
     // 3-4. drop-and-recompute edits and perturbation (lane 0, sequential)
@@ -485,8 +492,9 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
   int* elig = last + T;
   int* n_elig = elig + T;
   uint32_t* alive = reinterpret_cast<uint32_t*>(n_elig + 1);  // [T][W]: i < t <= last[i]
-  uint32_t* wbuf = alive + T * W + static_cast<size_t>(wid) * B * stride;
-  uint32_t* dm = alive + T * W + static_cast<size_t>(warps) * B * stride + wid * D * W;  // [D][W] ops per device
+  uint16_t* tq = reinterpret_cast<uint16_t*>(alive + T * W);     // [T*W]: t of word q
+  uint32_t* wbuf = alive + T * W + (T * W + 1) / 2 + static_cast<size_t>(wid) * B * stride;
+  uint32_t* dm = alive + T * W + (T * W + 1) / 2 + static_cast<size_t>(warps) * B * stride + wid * D * W;  // [D][W] ops per device
   for (int i = threadIdx.x; i < T * W; i += blockDim.x) cons[i] = 0u;
   for (int i = threadIdx.x; i < T; i += blockDim.x) last[i] = -1;
   __syncthreads();
@@ -501,7 +509,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
       if (last[j] > j + 1) elig[ne++] = j;
     *n_elig = ne;
   }
-  build_alive(alive, last, T, W);
+  build_alive(alive, tq, last, T, W);
   __syncthreads();
   const int n_el = *n_elig;
   for (int64_t k0 = (static_cast<int64_t>(blockIdx.x) * warps + wid) * B; k0 < a.n;
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
       __syncwarp();
       // 2. diagonal + minimal-save, word by word (measured faster here at
       // every cube size the batched kernel takes)
-      build_minimal_save(cube, dev, alive, dm, D, T, W, lane);
+      build_minimal_save(cube, dev, alive, tq, dm, D, T, W, lane);
     }
     // 3-4. one lane per candidate
     if (lane < nb) {
@@ -924,11 +932,11 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     const char* sc = std::getenv("XE_ROUND_SLOW_SCAN");
     a.slow_scan = sc && sc[0] == '1';
   }
-  const int smem = (2 * h.T * a.W32 + 2 * h.T + 1 + kRoundWarps * (words + h.T + h.D * a.W32)) * 4;
+  const int smem = (2 * h.T * a.W32 + (h.T * a.W32 + 1) / 2 + 2 * h.T + 1 + kRoundWarps * (words + h.T + h.D * a.W32)) * 4;
   int limit = 0;
   XE_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, pr->device));
   {  // lane per candidate when 32 cubes per warp fit (base cubes keep round_kernel)
-    const int tables = (2 * h.T * a.W32 + 2 * h.T + 1) * 4;  // cons, last, elig, n_elig, alive
+    const int tables = (2 * h.T * a.W32 + (h.T * a.W32 + 1) / 2 + 2 * h.T + 1) * 4;  // cons, last, elig, n_elig, alive, tq
     const char* e = std::getenv("XE_ROUND_BATCH");
     const int B = e ? std::max(0, std::min(32, std::atoi(e))) : 6;  // candidates per warp (0: round_kernel); 6 measured best
     const int per_warp = B * (words + h.T) * 4 + h.D * a.W32 * 4;
