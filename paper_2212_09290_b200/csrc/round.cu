@@ -87,6 +87,11 @@ struct RoundArgs {
   uint32_t* out;
   int word_build;  // steps 1-2 word by word (long-lived tensors) instead of one atomic per saved bit
   int slow_scan;   // XE_ROUND_SLOW_SCAN=1: the edits' backward row scans (test of the fast lookup)
+  // uniform placements (x null): per op the devices that can run it (cost
+  // below the sentinel) in order, their count, and the cheapest device
+  const uint8_t* ok_n;
+  const uint8_t* ok_list;  // [T][8]
+  const uint8_t* cheap;
 };
 
 constexpr int kRoundWarps = 4;
@@ -296,6 +301,47 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
 }
 
 
+// Step 1 for op i of candidate c: device drawn with probability proportional
+// to the LP diagonal x(R(d,i,i)) (uniform when x is null) over the devices
+// whose cost is below the sentinel, else the cheapest.  With x null the
+// draw is the floor(u * n)-th allowed device — what the running sum below
+// picks — read from the per-op tables.
+__device__ __forceinline__ int place_op(const RoundArgs& a, uint64_t c, int i) {
+  const int D = a.D, T = a.T;
+  if (!a.x && a.ok_n) {
+    const int n = a.ok_n[i];
+    if (n == 0) return a.cheap[i];
+    Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
+    const double u = rng.uniform() * n;
+    const int k = min(static_cast<int>(u), n - 1);
+    return a.ok_list[i * 8 + k];
+  }
+  Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
+  double tot = 0.0;
+  for (int d = 0; d < D; ++d) {
+    if (a.cost[d * T + i] >= 1.0e9) continue;
+    tot += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
+  }
+  int pick = 0;
+  if (tot == 0.0) {
+    double best = 1e300;  // every device prohibitive: cheapest
+    for (int d = 0; d < D; ++d)
+      if (a.cost[d * T + i] < best) best = a.cost[d * T + i], pick = d;
+  } else {
+    double u = rng.uniform() * tot, acc = 0.0;
+    int lastok = 0;
+    pick = -1;
+    for (int d = 0; d < D; ++d) {
+      if (a.cost[d * T + i] >= 1.0e9) continue;
+      acc += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
+      lastok = d;
+      if (pick < 0 && u < acc) pick = d;
+    }
+    if (pick < 0) pick = lastok;  // rounding tail
+  }
+  return pick;
+}
+
 // alive[t][w]: ops i of word w with i < t <= last[i] (the minimal-save set
 // of timestep t, candidate-independent); block-cooperative
 __device__ void build_alive(uint32_t* alive, uint16_t* tq, const int* last, int T, int W) {
@@ -435,30 +481,7 @@ __global__ void __launch_bounds__(kRoundWarps * 32) round_kernel(const RoundArgs
     }
     // 1. placement, one Philox stream per (candidate, op)
     for (int i = lane; i < T && !a.base; i += 32) {
-      Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
-      double tot = 0.0;
-      for (int d = 0; d < D; ++d) {
-        if (a.cost[d * T + i] >= 1.0e9) continue;
-        tot += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
-      }
-      int pick = 0;
-      if (tot == 0.0) {
-        double best = 1e300;  // every device prohibitive: cheapest
-        for (int d = 0; d < D; ++d)
-          if (a.cost[d * T + i] < best) best = a.cost[d * T + i], pick = d;
-      } else {
-        double u = rng.uniform() * tot, acc = 0.0;
-        int lastok = 0;
-        pick = -1;
-        for (int d = 0; d < D; ++d) {
-          if (a.cost[d * T + i] >= 1.0e9) continue;
-          acc += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
-          lastok = d;
-          if (pick < 0 && u < acc) pick = d;
-        }
-        if (pick < 0) pick = lastok;  // rounding tail
-      }
-      dev[i] = pick;
+      dev[i] = place_op(a, c, i);
     }
     __syncwarp();
     // 2. diagonal + minimal-save
@@ -521,30 +544,7 @@ __global__ void __launch_bounds__(256) round_batch_kernel(const RoundArgs a, int
       int* dev = reinterpret_cast<int*>(cube + words);
       // 1. placement, one Philox stream per (candidate, op)
       for (int i = lane; i < T; i += 32) {
-        Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
-        double tot = 0.0;
-        for (int d = 0; d < D; ++d) {
-          if (a.cost[d * T + i] >= 1.0e9) continue;
-          tot += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
-        }
-        int pick = 0;
-        if (tot == 0.0) {
-          double best = 1e300;
-          for (int d = 0; d < D; ++d)
-            if (a.cost[d * T + i] < best) best = a.cost[d * T + i], pick = d;
-        } else {
-          double u = rng.uniform() * tot, acc = 0.0;
-          int lastok = 0;
-          pick = -1;
-          for (int d = 0; d < D; ++d) {
-            if (a.cost[d * T + i] >= 1.0e9) continue;
-            acc += a.x ? fmax(a.x[a.r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3) : 1.0;
-            lastok = d;
-            if (pick < 0 && u < acc) pick = d;
-          }
-          if (pick < 0) pick = lastok;
-        }
-        dev[i] = pick;
+        dev[i] = place_op(a, c, i);
       }
       __syncwarp();
       // 2. diagonal + minimal-save, word by word (measured faster here at
@@ -920,6 +920,26 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.perturb = perturb;
   a.out = out;
   const int words = 2 * h.D * h.T * a.W32;
+  DevBuf<uint8_t> okn, okl, chp;
+  if (!a.x && h.D <= 8) {
+    std::vector<uint8_t> n(static_cast<size_t>(h.T)), l(static_cast<size_t>(h.T) * 8, 0), ch(static_cast<size_t>(h.T));
+    for (int i = 0; i < h.T; ++i) {
+      int k = 0, best = 0;
+      for (int d = 0; d < h.D; ++d) {
+        const double cd = h.cost[static_cast<size_t>(d) * h.T + i];
+        if (cd < 1.0e9) l[static_cast<size_t>(i) * 8 + k++] = static_cast<uint8_t>(d);
+        if (cd < h.cost[static_cast<size_t>(best) * h.T + i]) best = d;
+      }
+      n[static_cast<size_t>(i)] = static_cast<uint8_t>(k);
+      ch[static_cast<size_t>(i)] = static_cast<uint8_t>(best);
+    }
+    okn.upload(n, s);
+    okl.upload(l, s);
+    chp.upload(ch, s);
+    a.ok_n = okn.p;
+    a.ok_list = okl.p;
+    a.cheap = chp.p;
+  }
   {  // word-by-word steps 1-2 when the saved bits outnumber the cube's words
     int64_t saves = 0;
     std::vector<int> lastc(static_cast<size_t>(h.T), -1);
@@ -956,7 +976,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
         round_batch_kernel<<<grid, warps * 32, bsmem, s>>>(a, warps, B);
         XE_CUDA(cudaGetLastError());
       }
-      if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));
+      if (a.n_rc > 0 || a.ok_n) XE_CUDA(cudaStreamSynchronize(s));  // call-local tables
       return;
     }
   }
@@ -970,7 +990,7 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     round_kernel<<<grid, kRoundWarps * 32, smem, s>>>(a);
     XE_CUDA(cudaGetLastError());
   }
-  if (a.n_rc > 0) XE_CUDA(cudaStreamSynchronize(s));  // the recompute list above is call-local
+  if (a.n_rc > 0 || a.ok_n) XE_CUDA(cudaStreamSynchronize(s));  // the recompute list / device tables are call-local
 }
 
 // shared memory of the move kernel: consumer masks + per warp a cube and the
