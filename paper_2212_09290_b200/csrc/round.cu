@@ -92,6 +92,7 @@ struct RoundArgs {
   const uint8_t* ok_n;
   const uint8_t* ok_list;  // [T][8]
   const uint8_t* cheap;
+  const double* lp_cum;  // [T][8] running sums of max(x(R(d,i,i)), 1e-3) over the allowed devices (x given)
 };
 
 constexpr int kRoundWarps = 4;
@@ -301,6 +302,20 @@ __device__ void edit_candidate(const RoundArgs& a, uint32_t* cube, const int* de
 }
 
 
+// running sums of the LP weights over op i's allowed devices, in device
+// order (the additions place_op's general path makes, in the same order)
+__global__ void lp_cum_kernel(const double* x, int64_t r_base, const uint8_t* ok_n, const uint8_t* ok_list, int T,
+                              double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  double tot = 0.0;
+  for (int k = 0; k < ok_n[i]; ++k) {
+    const int d = ok_list[i * 8 + k];
+    tot += fmax(x[r_base + (static_cast<int64_t>(d) * T + i) * T + i], 1e-3);
+    out[i * 8 + k] = tot;
+  }
+}
+
 // Step 1 for op i of candidate c: device drawn with probability proportional
 // to the LP diagonal x(R(d,i,i)) (uniform when x is null) over the devices
 // whose cost is below the sentinel, else the cheapest.  With x null the
@@ -315,6 +330,16 @@ __device__ __forceinline__ int place_op(const RoundArgs& a, uint64_t c, int i) {
     const double u = rng.uniform() * n;
     const int k = min(static_cast<int>(u), n - 1);
     return a.ok_list[i * 8 + k];
+  }
+  if (a.x && a.lp_cum) {  // the same running sums, precomputed per op
+    const int n = a.ok_n[i];
+    if (n == 0) return a.cheap[i];
+    const double* cum = a.lp_cum + i * 8;
+    Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
+    const double u = rng.uniform() * cum[n - 1];
+    for (int k = 0; k < n; ++k)
+      if (u < cum[k]) return a.ok_list[i * 8 + k];
+    return a.ok_list[i * 8 + n - 1];  // rounding tail
   }
   Philox rng(a.seed, c, 0x10000u + static_cast<uint32_t>(i));
   double tot = 0.0;
@@ -921,7 +946,8 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
   a.out = out;
   const int words = 2 * h.D * h.T * a.W32;
   DevBuf<uint8_t> okn, okl, chp;
-  if (!a.x && h.D <= 8) {
+  DevBuf<double> lpc;
+  if (h.D <= 8) {
     std::vector<uint8_t> n(static_cast<size_t>(h.T)), l(static_cast<size_t>(h.T) * 8, 0), ch(static_cast<size_t>(h.T));
     for (int i = 0; i < h.T; ++i) {
       int k = 0, best = 0;
@@ -939,6 +965,12 @@ void round_cubes_device(const xe_problem* pr, const double* x, uint64_t seed, in
     a.ok_n = okn.p;
     a.ok_list = okl.p;
     a.cheap = chp.p;
+    if (a.x) {
+      lpc.alloc(static_cast<size_t>(h.T) * 8);
+      lp_cum_kernel<<<(h.T + 127) / 128, 128, 0, s>>>(a.x, a.r_base, okn.p, okl.p, h.T, lpc.p);
+      XE_CUDA(cudaGetLastError());
+      a.lp_cum = lpc.p;
+    }
   }
   {  // word-by-word steps 1-2 when the saved bits outnumber the cube's words
     int64_t saves = 0;
