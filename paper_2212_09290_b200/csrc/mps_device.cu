@@ -11,8 +11,9 @@
 // model can hold (costs, copy costs, energy terms and limits) are formatted
 // once on the host with the shortest round-trip rule and looked up by their
 // bits.  A value missing from that table (it cannot happen for models K1
-// builds) makes the caller fall back to the host writer.  QUADOBJ models use
-// the host writer.
+// builds) makes the caller fall back to the host writer.  QUADOBJ models
+// drop the P columns and P_LINK rows and add the QUADOBJ section, one item
+// per (t, e, ds, dc) with a nonzero copy cost.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -33,6 +34,10 @@ __constant__ char kTagC[14][13] = {"EQ7",     "EQ8",     "EQ9",    "EQ10",   "EQ
 
 struct Args {
   int64_t D, T, E, n_rows, n_cols, firstU;
+  int64_t ncol_out;  // columns written: all, or up to the first P column (QUADOBJ models)
+  int quad;          // QUADOBJ model: P columns and P_LINK rows dropped, a QUADOBJ section added
+  const int32_t *src, *dst;
+  const double* w;   // [E][D][D] copy costs
   const int8_t* sense;
   const uint8_t *tag, *present, *kind;
   const int32_t *ordinal, *crow;
@@ -148,10 +153,14 @@ __device__ void row_name(W& w, const Args& a, int64_t r) {
   w.i(a.ordinal[r]);
 }
 
-// section items: 0 ROWS (row r), 1 COLUMNS (column j), 2 RHS (row r), 3 BOUNDS (column j)
+constexpr uint8_t kPLink = 11;
+
+// section items: 0 ROWS (row r), 1 COLUMNS (column heads and entries), 2 RHS
+// (row r), 3 BOUNDS (column j), 4 QUADOBJ ((t, e, ds, dc) in loop order)
 template <int SEC>
 __device__ void item(W& w, const Args& a, int64_t k) {
   if (SEC == 0) {
+    if (a.quad && a.tag[k] == kPLink) return;
     w.c(' ');
     w.c(static_cast<char>(a.sense[k]));
     w.c(' ');
@@ -159,7 +168,7 @@ __device__ void item(W& w, const Args& a, int64_t k) {
     w.c('\n');
   } else if (SEC == 1) {
     // column j's head sits at col_ptr[j] + j, its entries follow
-    int64_t lo = 0, hi = a.n_cols - 1;
+    int64_t lo = 0, hi = a.ncol_out - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
       if (a.col_ptr[mid] + mid <= k) lo = mid;
@@ -178,6 +187,7 @@ __device__ void item(W& w, const Args& a, int64_t k) {
       }
     } else {
       const int64_t q = a.col_ptr[j] + (k - head - 1);
+      if (a.quad && a.tag[a.crow[q]] == kPLink) return;
       w.s("    ");
       col_name(w, a, j);
       w.s("  ");
@@ -188,11 +198,24 @@ __device__ void item(W& w, const Args& a, int64_t k) {
     }
   } else if (SEC == 2) {
     const double v = a.rhs[k];
-    if (v == 0.0) return;
+    if (v == 0.0 || (a.quad && a.tag[k] == kPLink)) return;
     w.s("    RHS  ");
     row_name(w, a, k);
     w.s("  ");
     num(w, a, v);
+    w.c('\n');
+  } else if (SEC == 4) {
+    const int64_t D = a.D, T = a.T, E = a.E;
+    const int64_t dc = k % D, ds = k / D % D, e = k / (D * D) % E, t = k / (D * D * E);
+    if (ds == dc) return;
+    const double wv = a.w[(e * D + ds) * D + dc];
+    if (wv == 0.0) return;
+    w.s("    ");
+    col_name(w, a, (dc * T + t) * T + a.dst[e]);
+    w.s("  ");
+    col_name(w, a, 2 * D * T * T + (ds * T + t) * T + a.src[e]);
+    w.s("  ");
+    num(w, a, wv);
     w.c('\n');
   } else {
     const uint8_t kd = a.kind[k];
@@ -259,11 +282,11 @@ inline unsigned grid_for(int64_t n) {
 }  // namespace mpsd
 
 // Leaves the text in m->mps_dev.  Returns false when the device writer
-// cannot serve the model (QUADOBJ, or a non-integral number outside the
-// host-formatted table): the caller then uses the host writer.
+// cannot serve the model (a non-integral number outside the host-formatted
+// table): the caller then uses the host writer.
 bool mps_text_device(xe_csr* m) {
   using namespace mpsd;
-  if (m->opts.quadratic_objective) return false;
+  const bool quad = m->opts.quadratic_objective != 0;
   const xe_csr_info& in = m->info;
   const HostProblem& h = m->prob->h;
   cudaStream_t s = m->stream;
@@ -321,6 +344,12 @@ bool mps_text_device(xe_csr* m) {
   a.n_rows = in.n_rows;
   a.n_cols = in.n_cols;
   a.firstU = 3ll * in.D * in.T * in.T + static_cast<int64_t>(in.D) * in.T * (in.E + in.T);
+  const int64_t firstP = a.firstU + static_cast<int64_t>(in.D) * in.T * in.T;
+  a.quad = quad ? 1 : 0;
+  a.ncol_out = quad ? std::min<int64_t>(firstP, in.n_cols) : in.n_cols;
+  a.src = m->prob->dev.src;
+  a.dst = m->prob->dev.dst;
+  a.w = m->prob->d_w.p;
   a.sense = m->sense.p;
   a.tag = m->tag.p;
   a.present = m->present.p;
@@ -337,24 +366,47 @@ bool mps_text_device(xe_csr* m) {
   a.npool = dpool.p;
   a.nnum = static_cast<int>(noff.size()) - 1;
   a.missing = missing.p;
-  const int64_t ns[4] = {in.n_rows, in.n_cols + in.nnz, in.n_rows, in.n_cols};
+  // column items: heads and entries of the columns written
+  int64_t col_items = in.n_cols + in.nnz;
+  if (a.ncol_out < in.n_cols) {
+    int64_t e_out = 0;
+    XE_CUDA(cudaMemcpyAsync(&e_out, m->col_ptr.p + a.ncol_out, 8, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaStreamSynchronize(s));
+    col_items = a.ncol_out + e_out;
+  }
+  bool any_quad = false;  // QUADOBJ lines exist (a nonzero cross-device copy cost)
+  if (quad)
+    for (int e = 0; e < h.E && !any_quad; ++e)
+      for (int x = 0; x < h.D && !any_quad; ++x)
+        for (int y = 0; y < h.D; ++y)
+          if (x != y && h.w[(static_cast<size_t>(e) * h.D + x) * h.D + y] != 0.0) {
+            any_quad = true;
+            break;
+          }
+  constexpr int kSec = 5;
+  const int64_t ns[kSec] = {in.n_rows, col_items, in.n_rows, a.ncol_out,
+                            any_quad ? static_cast<int64_t>(in.T) * in.E * in.D * in.D : 0};
   // the INTEND that closes a model without continuous columns follows the
   // last column item
-  const std::string sec_tail[4] = {"", a.firstU == in.n_cols && a.firstU > 0 ? "    MARK  'MARKER'  'INTEND'\n" : "", "", ""};
-  const char* const head[4] = {"NAME XENGINE\nROWS\n N OBJ\n", "COLUMNS\n", "RHS\n", "BOUNDS\n"};
+  const std::string sec_tail[kSec] = {
+      "", a.firstU == a.ncol_out && a.firstU > 0 ? "    MARK  'MARKER'  'INTEND'\n" : "", "", "", ""};
+  const char* const head[kSec] = {"NAME XENGINE\nROWS\n N OBJ\n", "COLUMNS\n", "RHS\n", "BOUNDS\n",
+                                  any_quad ? "QUADOBJ\n" : ""};
   // per section: lengths -> in-place inclusive scan -> offsets
-  std::vector<DevBuf<int64_t>> off(4);
-  std::vector<int64_t> bytes(4, 0);
-  for (int sec = 0; sec < 4; ++sec) {
+  std::vector<DevBuf<int64_t>> off(kSec);
+  std::vector<int64_t> bytes(kSec, 0);
+  for (int sec = 0; sec < kSec; ++sec) {
     const int64_t n = ns[sec];
     off[static_cast<size_t>(sec)].alloc(static_cast<size_t>(n) + 1);
     int64_t* o = off[static_cast<size_t>(sec)].p;
     XE_CUDA(cudaMemsetAsync(o, 0, 8, s));
+    if (n == 0) continue;
     switch (sec) {
       case 0: size_kernel<0><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
       case 1: size_kernel<1><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
       case 2: size_kernel<2><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
-      default: size_kernel<3><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
+      case 3: size_kernel<3><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
+      default: size_kernel<4><<<grid_for(n), kBlock, 0, s>>>(a, n, o + 1); break;
     }
     XE_CUDA(cudaGetLastError());
     thrust::inclusive_scan(thrust::cuda::par.on(s), o + 1, o + 1 + n, o + 1);
@@ -366,26 +418,29 @@ bool mps_text_device(xe_csr* m) {
   if (miss) return false;
   const std::string tail = "ENDATA\n";
   size_t total = tail.size();
-  for (int sec = 0; sec < 4; ++sec)
+  for (int sec = 0; sec < kSec; ++sec)
     total += std::strlen(head[sec]) + static_cast<size_t>(bytes[static_cast<size_t>(sec)]) + sec_tail[sec].size();
   DevBuf<char>& text = m->mps_dev;
   text.alloc(std::max<size_t>(1, total));
   m->mps_dev_len = total;
   size_t at = 0;
-  for (int sec = 0; sec < 4; ++sec) {
+  for (int sec = 0; sec < kSec; ++sec) {
     const size_t hl = std::strlen(head[sec]);
-    XE_CUDA(cudaMemcpyAsync(text.p + at, head[sec], hl, cudaMemcpyHostToDevice, s));
+    if (hl) XE_CUDA(cudaMemcpyAsync(text.p + at, head[sec], hl, cudaMemcpyHostToDevice, s));
     at += hl;
     char* base = text.p + at;
     const int64_t n = ns[sec];
     const int64_t* o = off[static_cast<size_t>(sec)].p;
-    switch (sec) {
-      case 0: write_kernel<0><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
-      case 1: write_kernel<1><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
-      case 2: write_kernel<2><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
-      default: write_kernel<3><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+    if (n > 0) {
+      switch (sec) {
+        case 0: write_kernel<0><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+        case 1: write_kernel<1><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+        case 2: write_kernel<2><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+        case 3: write_kernel<3><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+        default: write_kernel<4><<<grid_for(n), kBlock, 0, s>>>(a, n, o, base); break;
+      }
+      XE_CUDA(cudaGetLastError());
     }
-    XE_CUDA(cudaGetLastError());
     at += static_cast<size_t>(bytes[static_cast<size_t>(sec)]);
     if (!sec_tail[sec].empty()) {
       XE_CUDA(cudaMemcpyAsync(text.p + at, sec_tail[sec].data(), sec_tail[sec].size(), cudaMemcpyHostToDevice, s));
