@@ -22,8 +22,10 @@ for name, doc, n in (("fig2", fig2, 300), ("vgg16", configs.vgg16_doc(), 2048), 
     p = xe.Problem.from_json(doc)
     m = xe.build_model(p)
     m.write_mps()                                         # device MPS emission
+    xe.build_model(p, xe.ModelOptions(quadratic_objective=True)).write_mps()  # QUADOBJ
     m.csc()
-    xe.pdhg_solve(m, tol=1e-3, max_iters=256)
+    lp = xe.pdhg_solve(m, tol=1e-3, max_iters=256, return_x=True)
+    xe.round_cubes(p, min(n, 512), 9, edits=3, perturb=0.1, x=torch.from_numpy(lp.x).cuda())  # LP-guided K4
     cubes = xe.round_cubes(p, n, 7, edits=3, perturb=0.1)
     nb = xe.move_cubes(p, cubes[:4], 64, 3, max_moves=3)
     r = xe.evaluate_cubes(p, cubes)                       # streaming (fast) path + refine
