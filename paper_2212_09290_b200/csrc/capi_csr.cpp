@@ -3,6 +3,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+#include <algorithm>
 
 #include <sys/mman.h>
 
@@ -20,7 +24,50 @@ constexpr uintptr_t kHuge = uintptr_t(2) << 20;
 }  // namespace
 int64_t check_rows_host(xe_csr* m, const double* x_host, double tol, double* viol_host);  // complete.cu
 
-// the host writer (mps_writer.cpp): QUADOBJ models, XE_MPS_HOST=1
+// Device -> pageable host download of a large text: chunks go through two
+// pinned staging buffers (the next chunk's copy overlaps this one's) and
+// are spread into the destination by several host threads, so its first-
+// touch page faults are taken in parallel.  Small texts: one plain copy.
+void download_parallel(char* dst, const char* src, size_t n, cudaStream_t s) {
+  constexpr size_t kChunk = size_t(32) << 20;
+  static std::mutex mu;
+  static char* stage[2] = {nullptr, nullptr};
+  static cudaEvent_t ev[2];
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < 2 * kChunk || hw < 2) {
+    XE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if (!stage[0]) {
+    for (int b = 0; b < 2; ++b) {
+      XE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk));
+      XE_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+  }
+  const size_t nch = (n + kChunk - 1) / kChunk;
+  auto issue = [&](size_t k) {
+    const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+    XE_CUDA(cudaMemcpyAsync(stage[k & 1], src + off, len, cudaMemcpyDeviceToHost, s));
+    XE_CUDA(cudaEventRecord(ev[k & 1], s));
+  };
+  issue(0);
+  for (size_t k = 0; k < nch; ++k) {
+    XE_CUDA(cudaEventSynchronize(ev[k & 1]));
+    if (k + 1 < nch) issue(k + 1);  // into the other buffer, free since chunk k-1 was spread
+    const size_t off = k * kChunk, len = std::min(kChunk, n - off);
+    const size_t part = (len + hw - 1) / hw;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < hw; ++t) {
+      const size_t a = std::min(len, t * part), b = std::min(len, a + part);
+      if (b > a) th.emplace_back([=] { std::memcpy(dst + off + a, stage[k & 1] + a, b - a); });
+    }
+    for (auto& x : th) x.join();
+  }
+}
+
+// the host writer (mps_writer.cpp): the fallback, XE_MPS_HOST=1
 void mps_host(xe_csr* m) {
   build_csc(m, m->stream);
   cudaStream_t s = m->stream;
@@ -237,8 +284,7 @@ int xe_write_mps(xe_csr* m, char* buf, size_t* len) {
       const uintptr_t lo = (reinterpret_cast<uintptr_t>(buf) + kHuge - 1) & ~(kHuge - 1);
       const uintptr_t hi = (reinterpret_cast<uintptr_t>(buf) + n) & ~(kHuge - 1);
       if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
-      XE_CUDA(cudaMemcpyAsync(buf, m->mps_dev.p, n, cudaMemcpyDeviceToHost, m->stream));
-      XE_CUDA(cudaStreamSynchronize(m->stream));
+      download_parallel(buf, m->mps_dev.p, n, m->stream);
     } else {
       std::memcpy(buf, m->mps.data(), n);
     }
