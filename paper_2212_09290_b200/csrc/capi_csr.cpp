@@ -31,8 +31,7 @@ int64_t check_rows_host(xe_csr* m, const double* x_host, double tol, double* vio
 void download_parallel(char* dst, const char* src, size_t n, cudaStream_t s) {
   constexpr size_t kChunk = size_t(32) << 20;
   static std::mutex mu;
-  static char* stage[2] = {nullptr, nullptr};
-  static cudaEvent_t ev[2];
+  static char* stage[2] = {nullptr, nullptr};  // pinned host memory: usable from every device
   const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
   if (n < 2 * kChunk || hw < 2) {
     XE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
@@ -40,12 +39,18 @@ void download_parallel(char* dst, const char* src, size_t n, cudaStream_t s) {
     return;
   }
   std::lock_guard<std::mutex> lk(mu);
-  if (!stage[0]) {
-    for (int b = 0; b < 2; ++b) {
-      XE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk));
-      XE_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+  if (!stage[0])
+    for (int b = 0; b < 2; ++b) XE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk));
+  // events of the stream's device, per call
+  struct Events {
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
     }
-  }
+  } evs;
+  for (auto& x : evs.e) XE_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  cudaEvent_t* ev = evs.e;
   const size_t nch = (n + kChunk - 1) / kChunk;
   auto issue = [&](size_t k) {
     const size_t off = k * kChunk, len = std::min(kChunk, n - off);
