@@ -617,6 +617,22 @@ def main():
                        "h2d_bytes_per_step": ne * cube_bytes, "d2h_bytes_per_step": 24 * ((ne + (1 << 20) - 1) // (1 << 20)),
                        "candidates_per_step": ne, "path": "xe_eval_cubes_host (canonical cubes in a pinned host buffer; 2-stream chunked H2D, on-device transpose, lane-per-candidate evaluator)"}
         assert re.best_index == -1 or re.best_index < ne
+        # the same call returning every candidate's objective, peaks and flags
+        # to host arrays (the complete per-candidate contract of xe_eval_cubes)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ro = xe.evaluate_cubes_host(prob, hnp, outputs=True)
+            ts.append(time.perf_counter() - t0)
+        eo = float(np.median(ts))
+        to = torch.tensor([eo], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(to, op=dist.ReduceOp.MAX)
+        line["e2e_outputs"] = {"value": world * ne / float(to[0]), "unit": UNIT, "h2d_bytes_per_step": ne * cube_bytes,
+                               "d2h_bytes_per_step": ne * (8 + 8 * D + 4), "candidates_per_step": ne,
+                               "path": "xe_eval_cubes_host with per-candidate objective, peaks and flags copied to host arrays"}
+        assert ro.best_index == re.best_index
 
     # ---- K1 + K3 on the same config: GPU model assembly, PDHG LP relaxation ----
     if rank == 0 and not args.skip_pdhg:

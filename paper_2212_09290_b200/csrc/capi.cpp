@@ -466,10 +466,38 @@ static void eval_host_chunks(const xe_problem* p, const xe_model_opts& o, const 
   // the two stages' streams must not start before work already queued on
   // the handle's stream (previous calls) has finished with the buffers
   XE_CUDA(cudaStreamSynchronize(p->stream));
+  // outputs: chunk c's results land in its stage's pinned buffer and are
+  // copied to the caller's arrays once that stage comes round again
+  const bool want = out && (out->obj || out->peak || out->flags);
+  const size_t ob = static_cast<size_t>(cap) * (8 + 8 * static_cast<size_t>(h.D) + 4);
+  if (want)
+    for (auto& st : mp->stage)
+      if (st.pinned_bytes < ob) {
+        if (st.pinned) XE_CUDA(cudaFreeHost(st.pinned));
+        st.pinned = nullptr;
+        XE_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.pinned), ob));
+        st.pinned_bytes = ob;
+      }
+  auto stage_obj = [&](xe_problem::Stage& st) { return reinterpret_cast<double*>(st.pinned); };
+  auto stage_peak = [&](xe_problem::Stage& st) { return reinterpret_cast<int64_t*>(st.pinned + static_cast<size_t>(cap) * 8); };
+  auto stage_fl = [&](xe_problem::Stage& st) {
+    return reinterpret_cast<uint32_t*>(st.pinned + static_cast<size_t>(cap) * (8 + 8 * static_cast<size_t>(h.D)));
+  };
+  auto deliver = [&](int64_t c) {  // after stage (c & 1)'s stream finished chunk c
+    auto& st = mp->stage[c & 1];
+    const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+    if (out->obj) std::memcpy(out->obj + lo, stage_obj(st), static_cast<size_t>(m) * 8);
+    if (out->peak) std::memcpy(out->peak + lo * h.D, stage_peak(st), static_cast<size_t>(m) * h.D * 8);
+    if (out->flags) std::memcpy(out->flags + lo, stage_fl(st), static_cast<size_t>(m) * 4);
+  };
   try {
     for (int64_t c = 0; c < nchunks; ++c) {
       auto& st = mp->stage[c & 1];
       const int64_t lo = c * chunk, m = std::min(chunk, n - lo);
+      if (want && c >= 2) {
+        XE_CUDA(cudaStreamSynchronize(st.stream));
+        deliver(c - 2);
+      }
       uint64_t* b3 = mp->chunk_best.p + 3 * c;
       h2d(st.canon.p, reinterpret_cast<const unsigned char*>(cubes) + lo * cb, static_cast<size_t>(m) * cb,
           st.stream);
@@ -488,16 +516,17 @@ static void eval_host_chunks(const xe_problem* p, const xe_model_opts& o, const 
         eval_cubes_device(p, o, st.canon.p, m, o_obj, st.peak.p, o_fl, valid_mask, b3, st.scratch.p, st.stream);
       }
       if (out && out->obj)
-        XE_CUDA(cudaMemcpyAsync(out->obj + lo, st.obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st.stream));
+        XE_CUDA(cudaMemcpyAsync(stage_obj(st), st.obj.p, m * sizeof(double), cudaMemcpyDeviceToHost, st.stream));
       if (out && out->peak)
-        XE_CUDA(cudaMemcpyAsync(out->peak + lo * h.D, st.peak.p, m * h.D * sizeof(int64_t), cudaMemcpyDeviceToHost,
+        XE_CUDA(cudaMemcpyAsync(stage_peak(st), st.peak.p, m * h.D * sizeof(int64_t), cudaMemcpyDeviceToHost,
                                 st.stream));
       if (out && out->flags)
-        XE_CUDA(cudaMemcpyAsync(out->flags + lo, st.flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                                st.stream));
+        XE_CUDA(cudaMemcpyAsync(stage_fl(st), st.flags.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, st.stream));
     }
     XE_CUDA(cudaStreamSynchronize(mp->stage[0].stream));
     XE_CUDA(cudaStreamSynchronize(mp->stage[1].stream));
+    if (want)
+      for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) deliver(c);
   } catch (...) {
     cudaStreamSynchronize(mp->stage[0].stream);
     cudaStreamSynchronize(mp->stage[1].stream);

@@ -224,6 +224,14 @@ struct xe_problem {
     xe::DevBuf<uint8_t> scratch;
     xe::RefineBuf refine;
     cudaStream_t stream = nullptr;
+    // pinned host staging of a chunk's outputs (xe_eval_cubes_host): the
+    // device->host copies stay asynchronous, the caller's arrays are filled
+    // from here while later chunks run
+    unsigned char* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    ~Stage() {
+      if (pinned) cudaFreeHost(pinned);
+    }
   };
   Stage stage[2];
   xe::DevBuf<uint64_t> chunk_best;  // [chunks][3] best-of-chunk triples
