@@ -363,6 +363,19 @@ int xe_move_placements(const xe_problem* p, const uint8_t* base_dev, int64_t n_b
  * (seed, first + k) — the input family of config 5's placement sweep. */
 int xe_random_placements(const xe_problem* p, uint64_t seed, int64_t first, int64_t n, uint8_t* dev_out,
                          void* stream);
+/* One iteration of the placement local search's chain control, on the device
+ * (all buffers device): `chains` chains, each with `chain_n` scored
+ * neighbours nb[chains*chain_n][T] (obj / flags from xe_eval_placements).
+ * Per chain: its best neighbour (score = obj when (flags & valid_mask) == 0,
+ * else +inf; first index among equals) replaces bases[c] and cur[c] when it
+ * improves, or after `stall` iterations without improvement when valid;
+ * stalled[c] counts.  Then the lowest cur (first chain among equals)
+ * replaces *best / best_dev[T] when strictly lower, ++*improvements.  No
+ * host synchronisation. */
+int xe_placement_chains_step(const xe_problem* p, const double* obj, const uint32_t* flags, uint32_t valid_mask,
+                             const uint8_t* nb, int32_t chains, int32_t chain_n, int32_t stall, uint8_t* bases,
+                             double* cur, int32_t* stalled, double* best, uint8_t* best_dev, int32_t* improvements,
+                             void* stream);
 
 /* ---- best-schedule search (K1 -> K3 -> K4 -> K2, one native call) ------
  * The GPU counterpart of solve_exact / solve_external (solver.hpp:49-58):

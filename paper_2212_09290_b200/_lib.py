@@ -202,6 +202,8 @@ SIGNATURES = {
     "xe_mutate_cubes": (C.c_int, [P, P, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_double, P, P]),
     "xe_move_cubes": (C.c_int, [P, P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, P, P]),
     "xe_move_placements": (C.c_int, [P, P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, P, P]),
+    "xe_placement_chains_step": (C.c_int, [P, P, P, C.c_uint32, P, C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P,
+                                            P, P]),
     "xe_random_placements": (C.c_int, [P, C.c_uint64, C.c_int64, C.c_int64, P, P]),
     "xe_round_cubes": (C.c_int, [P, P, C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_double,
                                  P, P]),

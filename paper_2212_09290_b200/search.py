@@ -38,6 +38,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
+from ._lib import LIB
 from .api import ModelOptions, Problem, check
 
 # a schedule is usable when check_assignment passes, every device stays
@@ -152,6 +153,7 @@ def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 2
     each iteration scores chains x chain_n neighbours exactly (K2b) and a
     chain moves to its best valid neighbour when it improves, or after
     `stall` iterations without improvement."""
+    import ctypes as C
     import torch
     from .api import evaluate_placements, move_placements, random_placements
     dev = random_placements(problem, n_random, seed)
@@ -175,27 +177,27 @@ def search_placements(problem: Problem, n_random: int = 1 << 22, chains: int = 2
     del dev, r, score
     P, M = chains, chain_n
     stalled = torch.zeros(P, dtype=torch.int32, device="cuda")
-    rows = torch.arange(P, device="cuda") * M
-    best = float(cur.min().item())
-    best_dev = bases[int(torch.argmin(cur))].clone()
-    improvements, n_eval = 0, n_random
+    k0 = int(torch.argmin(cur))
+    best = cur[k0:k0 + 1].clone()            # device scalar: the incumbent
+    best_dev = bases[k0].clone()
+    improvements = torch.zeros(1, dtype=torch.int32, device="cuda")
+    n_eval = n_random
     nb = torch.empty((P * M, problem.T), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
     for it in range(iters):
         move_placements(problem, bases, P * M, seed ^ 0x9E3779B9, first=it * P * M, max_moves=max_moves, out=nb)
         r = evaluate_placements(problem, nb, policy=policy, valid_mask=valid_mask, best=False)
         n_eval += P * M
-        s = torch.where((r.flags & valid_mask) == 0, r.obj, torch.full_like(r.obj, float("inf"))).view(P, M)
-        v, j = s.min(1)
-        take = (v < cur) | ((stalled >= stall) & torch.isfinite(v))
-        bases = torch.where(take[:, None], nb[rows + j], bases)
-        stalled = torch.where(v < cur, torch.zeros_like(stalled), torch.where(take, torch.zeros_like(stalled),
-                                                                               stalled + 1))
-        cur = torch.where(take, v, cur)
-        b = float(cur.min().item())
-        if b < best:
-            best, best_dev = b, bases[int(torch.argmin(cur))].clone()
-            improvements += 1
-        del r, s
+        # chain control on the device (xe_placement_chains_step): no host sync per iteration
+        check(LIB.xe_placement_chains_step(problem.handle, C.c_void_p(r.obj.data_ptr()),
+                                           C.c_void_p(r.flags.data_ptr()), valid_mask, C.c_void_p(nb.data_ptr()),
+                                           P, M, stall, C.c_void_p(bases.data_ptr()), C.c_void_p(cur.data_ptr()),
+                                           C.c_void_p(stalled.data_ptr()), C.c_void_p(best.data_ptr()),
+                                           C.c_void_p(best_dev.data_ptr()), C.c_void_p(improvements.data_ptr()),
+                                           C.c_void_p(stream)))
+        del r
+    best = float(best.item())
+    improvements = int(improvements.item())
     r1 = evaluate_placements(problem, best_dev.unsqueeze(0).contiguous(), policy=policy, valid_mask=valid_mask)
     assert r1.best_obj == best, (r1.best_obj, best)
     return PlacementSearchResult(best, best_dev.cpu().numpy(), r1.peak.cpu().numpy()[0], rand_best, n_eval,
